@@ -1,0 +1,205 @@
+/*
+ * lbm_b200.h - C-ABI of the B200-native lattice Boltzmann hot path.
+ *
+ * This is the drop-in boundary for the reference's kernel slot
+ * (blocksim._kernels.impl, pkg/src/blocksim/_kernels/__init__.py:10-37) and
+ * for the sweep that drives it (lbm/sweep.py:93-151).  Every entry point
+ * takes raw device pointers, explicit geometry and a cudaStream_t passed as
+ * void*, returns 0 on success and a negative status otherwise
+ * (lbm_last_error() then holds the message).  No C++ exception crosses the
+ * boundary and nothing here allocates persistent device memory: the caller
+ * (Python/torch) owns every buffer.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/blocksim):
+ *   lbm_fused_step      impl.collide (_kernels/_core_py.py:70-200)
+ *                       + impl.stream_pull (_core_py.py:203-218)
+ *                       + BoundaryHandling.apply (lbm/boundary.py:154-195),
+ *                       fused as pull -> bounce-back -> collide (G-form).
+ *   lbm_collide_only    impl.collide on a freshly written R-form field
+ *                       (first half of the first stream_collide, sweep.py:147).
+ *   lbm_stream_only     impl.stream_pull + BoundaryHandling.apply without the
+ *                       following collide: turns the stored G-form back into
+ *                       the reference's R-form for readout (sweep.py:148-150).
+ *   lbm_moments         macroscopic / macroscopic_fields
+ *                       (lbm/collision.py:157-184, lbm/sweep.py:154-176).
+ *   lbm_fill_equilibrium  fill_equilibrium -> equilibrium
+ *                       (lbm/sweep.py:51-76, lbm/collision.py:138-154).
+ *   lbm_pack_rform / lbm_unpack_rform  Field.raw <-> device layout
+ *                       (field/core.py:34-70; "fzyx" raw shape (q,Z,Y,X)).
+ *   lbm_build_cellmask  build_index_lists + sweep-time flag validation
+ *                       (lbm/boundary.py:48-97, lbm/sweep.py:124-136).
+ *   lbm_collide_cells / lbm_equilibrium_cells / lbm_macroscopic_cells
+ *                       collide_pdfs / equilibrium / macroscopic on flat
+ *                       (n, q) populations (lbm/collision.py:138-184,245-261).
+ *   lbm_face_span       geometry of the per-step z-face ghost exchange
+ *                       (field/ghost.py:112-173,202-264), restricted to the
+ *                       PDF directions that cross the face.
+ *
+ * Device PDF layout ("z-q-y-x", one box per rank, one ghost layer on every
+ * side):  element (z, slot, y, x) lives at
+ *     ((z+1) * q + slot) * plane + (y+1) * pitch + xoff + x
+ * with plane = (ny+2) * pitch.  Direction i is stored in slot
+ * lbm_slot_of(q, i): slots are grouped by c_z (-1, 0, +1), so the directions
+ * that cross a z-face form ONE contiguous run per z-plane and the halo can be
+ * sent straight out of / into the field (zero-copy NCCL send/recv).
+ * real_bytes == 8 stores f in fp64; real_bytes == 4 stores (f - w_i) in fp32
+ * and computes in fp64 registers.
+ */
+#ifndef LBM_B200_H
+#define LBM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBM_B200_ABI_VERSION 1
+
+/* status codes */
+#define LBM_OK 0
+#define LBM_EINVAL -1    /* bad argument (maps to ValidationError) */
+#define LBM_ECUDA -2     /* CUDA launch/runtime failure */
+#define LBM_ENUMERIC -3  /* non-positive density (maps to NumericsError) */
+#define LBM_EFLAGS -4    /* flag validation failed (maps to ValidationError) */
+
+/* z-face modes of a rank's box */
+#define LBM_ZFACE_GHOST 0 /* domain face, non-periodic: ghost keeps its init value */
+#define LBM_ZFACE_HALO 1  /* ghost plane filled by the per-step exchange       */
+#define LBM_ZFACE_WRAP 2  /* periodic and owned by this rank: index wrap       */
+
+/* collision models (SRT.mode/TRT.mode/MRT.mode, lbm/collision.py:54,71,103) */
+#define LBM_SRT 0
+#define LBM_TRT 1
+#define LBM_MRT 2
+/* force models (Guo.mode / SimpleShift.mode, lbm/collision.py:115,128) */
+#define LBM_FORCE_NONE 0
+#define LBM_FORCE_GUO 1
+#define LBM_FORCE_SHIFT 2
+
+/* cell-mask bits written by lbm_build_cellmask */
+#define LBM_MASK_FLUID 0x1u        /* bit 0: cell is collided              */
+#define LBM_MASK_UBB 0x80000000u   /* bit 31: some link of the cell is UBB */
+#define LBM_MASK_PRESSURE 0x40000000u /* bit 30: some link is Pressure      */
+/* bits 1..q-1: pulled direction i comes from a boundary cell, i.e. the
+ * reference link (x, opp(i)) exists (boundary.py:91-95). */
+
+typedef struct lbm_grid {
+    int q;          /* 9, 19 or 27                                  */
+    int real_bytes; /* 8 (fp64) or 4 (fp32 storage of f - w_i)      */
+    int nx, ny, nz; /* interior cells of this rank's box            */
+    int pitch;      /* elements per x row (>= xoff + nx + 1)        */
+    int xoff;       /* element offset of interior x = 0 in a row (>= 1) */
+    int wrap_x;     /* 1: x periodic (index wrap), 0: ghost column  */
+    int wrap_y;     /* 1: y periodic (index wrap), 0: ghost row     */
+    int zface_lo;   /* LBM_ZFACE_* for the z = -1 side              */
+    int zface_hi;   /* LBM_ZFACE_* for the z = nz side              */
+} lbm_grid_t;
+
+typedef struct lbm_params {
+    int model;       /* LBM_SRT / LBM_TRT / LBM_MRT                    */
+    int force_mode;  /* LBM_FORCE_*                                    */
+    /* SRT (collision.py:130-136): rem = 1 - omega, hw = 1 - 0.5 omega  */
+    double omega, rem, hw;
+    /* TRT (collision.py:137-148,184-190): he_half = (1 - 0.5 w_e) * 0.5 */
+    double omega_e, omega_o, he_half, ho_half;
+    /* force: half_f = 0.5 * F (Guo) or tau * F (SimpleShift)           */
+    double fx, fy, fz;
+    double shift_fx, shift_fy, shift_fz;
+    /* UBB link constant per link direction k (the direction pointing INTO
+     * the wall): ((6 w_k) rho_0) (c_k . u_w) (boundary.py:165-170)     */
+    double ubb[27];
+    /* Pressure link constant per link direction k: (2 w_k) rho_w
+     * (boundary.py:171-195)                                             */
+    double pressure[27];
+    /* MRT tables, host pointer, row-major fp64 (collision.py:150-169,
+     * 192-197): M[q*q], Minv[q*q], S[q], G[q*q] (G only for Guo).  NULL
+     * unless model == LBM_MRT.                                          */
+    const double* mrt;
+} lbm_params_t;
+
+/* ------------------------------------------------------------- metadata */
+int lbm_abi_version(void);
+const char* lbm_last_error(void);
+/* storage slot of reference direction i (layout above); -1 on bad input */
+int lbm_slot_of(int q, int i);
+/* bytes of one PDF field in the device layout for this grid */
+int64_t lbm_field_elems(const lbm_grid_t* g);
+/* Span of the z-face exchange, in elements from the field base.
+ * face: 0 = low z face, 1 = high z face.
+ * recv: ghost-plane run this rank receives on that face (directions whose
+ *       c_z points into the box);
+ * send: interior boundary-plane run this rank sends through that face
+ *       (directions whose c_z points out of the box, i.e. into the peer). */
+int lbm_face_span(const lbm_grid_t* g, int face, int64_t* send_off,
+                  int64_t* recv_off, int64_t* count);
+
+/* ------------------------------------------------------------ hot path */
+/* One fused step on interior planes [z_begin, z_end): pull from G_n (src,
+ * ghosts valid), bounce-back on masked links, collide fluid cells, store
+ * G_{n+1} into dst.  cellmask: (nz, ny, nx) uint32 from lbm_build_cellmask;
+ * typemask: (nz, ny, nx, 2) uint32 - word 0 UBB link bits, word 1 Pressure
+ * link bits - only read where LBM_MASK_UBB / LBM_MASK_PRESSURE is set. */
+int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p,
+                   const void* src, void* dst, const uint32_t* cellmask,
+                   const uint32_t* typemask, int z_begin, int z_end,
+                   void* stream);
+
+/* Collide, in place, every interior cell whose cellmask has LBM_MASK_FLUID
+ * (G_0 = C(R_0)). */
+int lbm_collide_only(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,
+                     const uint32_t* cellmask, void* stream);
+
+/* R = S(G): pull + bounce-back without collision, written as dense fp64
+ * (q, nz, ny, nx) in reference direction order (host "fzyx" interior). */
+int lbm_stream_only(const lbm_grid_t* g, const lbm_params_t* p,
+                    const void* src, const uint32_t* cellmask,
+                    const uint32_t* typemask, double* out, void* stream);
+
+/* rho (nz,ny,nx) and u (nz,ny,nx,3) of R = S(G) (stream_form = 1) or of the
+ * stored field itself (stream_form = 0, field holds R-form).  The Guo
+ * half-shift is applied when p->force_mode == LBM_FORCE_GUO.  Sets
+ * *bad_count (device int) to the number of cells with rho <= 0. */
+int lbm_moments(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
+                const uint32_t* cellmask, const uint32_t* typemask,
+                int stream_form, double* rho, double* u, int* bad_count,
+                void* stream);
+
+/* Dense fp64 (q, Z, Y, X) ghost-inclusive R-form (Z=nz+2, ...) -> layout. */
+int lbm_pack_rform(const lbm_grid_t* g, const double* dense, void* pdf,
+                   void* stream);
+/* layout -> dense fp64 (q, Z, Y, X) ghost-inclusive (no streaming). */
+int lbm_unpack_rform(const lbm_grid_t* g, const void* pdf, double* dense,
+                     void* stream);
+/* Equilibrium of rho (Z,Y,X) and u (Z,Y,X,3), ghost-inclusive, into the
+ * layout (R-form) - equilibrium() op order (collision.py:150-154). */
+int lbm_fill_equilibrium(const lbm_grid_t* g, const double* rho,
+                         const double* u, void* pdf, void* stream);
+
+/* Flag validation + link masks from ghost-inclusive flags (Z, Y, X) uint32.
+ * bits: [0]=Fluid [1]=NoSlip [2]=UBB [3]=Pressure [4]=Solid registry masks.
+ * err (device int[8], caller zeroes): [0] first conflicting cell + 1,
+ * [1] first fluid cell pulling from Solid + 1, [2] first fluid cell pulling
+ * from an unflagged cell + 1, [3] first unflagged interior cell + 1,
+ * [4] number of UBB links, [5] number of NoSlip links, [6] number of
+ * Pressure links, [7] first fluid cell pulling from an uncovered Fluid
+ * ghost + 1 (unsupported: such ghosts would collide every step in the
+ * reference but are never refreshed).  Linear indices are z*ny*nx + y*nx + x (interior). */
+int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags,
+                       const uint32_t bits[5], uint32_t* cellmask,
+                       uint32_t* typemask, int* err, void* stream);
+
+/* ----------------------------------------- flat-cell utilities (n, q) */
+int lbm_collide_cells(int q, const lbm_params_t* p, double* f, int64_t n,
+                      void* stream);
+int lbm_equilibrium_cells(int q, const double* rho, const double* u,
+                          double* f, int64_t n, void* stream);
+int lbm_macroscopic_cells(int q, const lbm_params_t* p, const double* f,
+                          double* rho, double* u, int* bad_count, int64_t n,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBM_B200_H */

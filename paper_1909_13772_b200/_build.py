@@ -1,0 +1,100 @@
+"""In-tree build of the sm_100a kernel library and the CPU oracle.
+
+`build_all()` is what `__graft_entry__.build()` runs: nvcc compiles every
+CUDA unit for sm_100a (`-gencode arch=compute_100a,code=sm_100a -lineinfo`)
+into `paper_1909_13772_b200/_lbm_b200.so`, and gcc builds the test-only
+oracle `oracle/build/liblbm_oracle.so`.  Both land in the source tree so the
+snapshot that `gpurun` ships carries them (they are git-ignored).
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "_lbm_b200.so"
+OBJ = PKG / "build"
+ORACLE_DIR = ROOT / "oracle"
+ORACLE_LIB = ORACLE_DIR / "build" / "liblbm_oracle.so"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+               "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+# (source, extra flags): the fp64 unit and the C-ABI unit keep every
+# floating-point operation separately rounded (-fmad=false) for bitwise parity
+# with the reference; the fp32-storage unit may contract to FMA.
+UNITS = [
+    ("lbm_inst_f64.cu", ["-fmad=false"]),
+    ("lbm_inst_f32.cu", ["-fmad=true"]),
+    ("lbm_capi.cu", ["-fmad=false"]),
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found: the B200 kernel library cannot be built")
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def _run(cmd, log=None):
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if log is not None:
+        log.write(" ".join(cmd) + "\n" + res.stdout + res.stderr + "\n")
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build step failed: {' '.join(cmd[:4])} ...")
+    return res
+
+
+def build_kernels(force: bool = False, verbose: bool = False) -> Path:
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "lbm_b200.h"]
+    OBJ.mkdir(exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    with open(OBJ / "ptxas.log", "w") as log:
+        for src, extra in UNITS:
+            s = CSRC / src
+            o = OBJ / (Path(src).stem + ".o")
+            objs.append(o)
+            if force or _stale(o, [s, *headers]):
+                cmd = [nvcc, *ARCH, *NVCC_COMMON, *extra, "-I", str(ROOT / "include"),
+                       "-c", str(s), "-o", str(o)]
+                if verbose:
+                    print(" ".join(cmd), flush=True)
+                _run(cmd, log)
+        if force or _stale(LIB, objs):
+            _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"], log)
+    return LIB
+
+
+def build_oracle(force: bool = False) -> Path:
+    src = ORACLE_DIR / "lbm_oracle.c"
+    ORACLE_LIB.parent.mkdir(exist_ok=True)
+    if force or _stale(ORACLE_LIB, [src]):
+        # -ffp-contract=off: no FMA, same per-op rounding as numpy's ufuncs
+        _run(["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+              "-fno-fast-math", "-std=c11", "-o", str(ORACLE_LIB), str(src), "-lm"])
+    return ORACLE_LIB
+
+
+def build_all(force: bool = False, verbose: bool = False) -> None:
+    build_kernels(force=force, verbose=verbose)
+    if (ORACLE_DIR / "lbm_oracle.c").exists():
+        build_oracle(force=force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,115 @@
+"""ctypes binding of the sm_100a kernel library (include/lbm_b200.h).
+
+The library is loaded from the package directory (built in-tree by
+`_build.build_kernels`).  Every compute entry point of the package goes
+through `call()`, which maps status codes onto the reference's exception
+classes.  There is no fallback: a missing library or a failed launch raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from .errors import BackendError, NumericsError, ValidationError
+
+LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
+
+LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
+ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
+MASK_FLUID = 0x1
+MASK_UBB = 0x80000000
+
+# every symbol include/lbm_b200.h declares (tests check the export table)
+EXPORTS = (
+    "lbm_abi_version", "lbm_last_error", "lbm_slot_of", "lbm_field_elems", "lbm_face_span",
+    "lbm_fused_step", "lbm_collide_only", "lbm_stream_only", "lbm_moments",
+    "lbm_pack_rform", "lbm_unpack_rform", "lbm_fill_equilibrium", "lbm_build_cellmask",
+    "lbm_collide_cells", "lbm_equilibrium_cells", "lbm_macroscopic_cells",
+)
+
+
+class Grid(ctypes.Structure):
+    """lbm_grid_t"""
+    _fields_ = [("q", ctypes.c_int), ("real_bytes", ctypes.c_int), ("nx", ctypes.c_int),
+                ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("pitch", ctypes.c_int),
+                ("xoff", ctypes.c_int), ("wrap_x", ctypes.c_int), ("wrap_y", ctypes.c_int),
+                ("zface_lo", ctypes.c_int), ("zface_hi", ctypes.c_int)]
+
+
+class Params(ctypes.Structure):
+    """lbm_params_t"""
+    _fields_ = [("model", ctypes.c_int), ("force_mode", ctypes.c_int),
+                ("omega", ctypes.c_double), ("rem", ctypes.c_double), ("hw", ctypes.c_double),
+                ("omega_e", ctypes.c_double), ("omega_o", ctypes.c_double),
+                ("he_half", ctypes.c_double), ("ho_half", ctypes.c_double),
+                ("fx", ctypes.c_double), ("fy", ctypes.c_double), ("fz", ctypes.c_double),
+                ("shift_fx", ctypes.c_double), ("shift_fy", ctypes.c_double),
+                ("shift_fz", ctypes.c_double), ("ubb", ctypes.c_double * 27),
+                ("mrt", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load(path: Path | None = None):
+    """Load (once) and return the kernel library; raises BackendError."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise BackendError(
+            f"B200 kernel library {p} is missing; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+    lib = ctypes.CDLL(str(p))
+    P, I, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    G, PR = ctypes.POINTER(Grid), ctypes.POINTER(Params)
+    sig = {
+        "lbm_abi_version": ([], I),
+        "lbm_last_error": ([], ctypes.c_char_p),
+        "lbm_slot_of": ([I, I], I),
+        "lbm_field_elems": ([G], I64),
+        "lbm_face_span": ([G, I, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)], I),
+        "lbm_fused_step": ([G, PR, P, P, P, P, I, I, P], I),
+        "lbm_collide_only": ([G, PR, P, P, P], I),
+        "lbm_stream_only": ([G, PR, P, P, P, P, P], I),
+        "lbm_moments": ([G, PR, P, P, P, I, P, P, P, P], I),
+        "lbm_pack_rform": ([G, P, P, P], I),
+        "lbm_unpack_rform": ([G, P, P, P], I),
+        "lbm_fill_equilibrium": ([G, P, P, P, P], I),
+        "lbm_build_cellmask": ([G, P, P, P, P, P, P], I),
+        "lbm_collide_cells": ([I, PR, P, I64, P], I),
+        "lbm_equilibrium_cells": ([I, P, P, P, I64, P], I),
+        "lbm_macroscopic_cells": ([I, PR, P, P, P, P, I64, P], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.lbm_abi_version() != 1:
+        raise BackendError("kernel library ABI mismatch")
+    _lib = lib
+    return lib
+
+
+def call(name, *args):
+    """Invoke `name`, turning a non-zero status into the matching exception."""
+    lib = load()
+    st = getattr(lib, name)(*args)
+    if st != LBM_OK:
+        msg = (lib.lbm_last_error() or b"").decode(errors="replace")
+        if st == LBM_EINVAL or st == LBM_EFLAGS:
+            raise ValidationError(f"{name}: {msg}")
+        if st == LBM_ENUMERIC:
+            raise NumericsError(f"{name}: {msg}")
+        raise BackendError(f"{name}: {msg}")
+    return st
+
+
+def ptr(t) -> ctypes.c_void_p:
+    """Device pointer of a torch tensor (or None)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream) -> ctypes.c_void_p:
+    return ctypes.c_void_p(stream.cuda_stream)

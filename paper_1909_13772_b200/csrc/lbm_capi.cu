@@ -1,0 +1,505 @@
+// extern "C" boundary of the LBM hot path (declared in include/lbm_b200.h).
+//
+// Converts the plain-C geometry/parameter structs into kernel structs,
+// validates arguments, dispatches to the fp64 / fp32 instantiation units and
+// turns CUDA errors into status codes + a thread-local message.  Also hosts
+// the flag-validation / link-mask kernel and the flat-cell utilities
+// (compiled with -fmad=false like the fp64 unit).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/lbm_b200.h"
+#include "lbm_kernels.cuh"
+#include "lbm_launch.h"
+
+namespace lbm {
+LBM_DEFINE_MRT_SETTER(set_mrt_tables_capi)
+}
+
+using namespace lbm;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return LBM_OK;
+    if (e == cudaErrorInvalidValue)
+        return fail(LBM_EINVAL, "%s: unsupported configuration", what);
+    return fail(LBM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool q_ok(int q) { return q == 9 || q == 19 || q == 27; }
+
+int check_grid(const lbm_grid_t* g, KGrid* k) {
+    if (!g) return fail(LBM_EINVAL, "grid is NULL");
+    if (!q_ok(g->q)) return fail(LBM_EINVAL, "q must be 9, 19 or 27, got %d", g->q);
+    if (g->real_bytes != 8 && g->real_bytes != 4)
+        return fail(LBM_EINVAL, "real_bytes must be 8 or 4, got %d", g->real_bytes);
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1)
+        return fail(LBM_EINVAL, "box must be non-empty, got %dx%dx%d", g->nx, g->ny, g->nz);
+    if (g->xoff < 1 || g->pitch < g->xoff + g->nx + 1)
+        return fail(LBM_EINVAL, "pitch %d / xoff %d cannot hold %d cells + ghosts", g->pitch,
+                    g->xoff, g->nx);
+    if (g->zface_lo < 0 || g->zface_lo > 2 || g->zface_hi < 0 || g->zface_hi > 2)
+        return fail(LBM_EINVAL, "bad z-face mode");
+    if ((g->zface_lo == LBM_ZFACE_WRAP) != (g->zface_hi == LBM_ZFACE_WRAP))
+        return fail(LBM_EINVAL, "z wrap must apply to both faces");
+    if (g->ny + 2 > 65535 || g->nz + 2 > 65535)
+        return fail(LBM_EINVAL, "ny/nz too large for the launch grid");
+    k->nx = g->nx;
+    k->ny = g->ny;
+    k->nz = g->nz;
+    k->pitch = g->pitch;
+    k->xoff = g->xoff;
+    k->wrap_x = g->wrap_x ? 1 : 0;
+    k->wrap_y = g->wrap_y ? 1 : 0;
+    k->zlo = g->zface_lo;
+    k->zhi = g->zface_hi;
+    k->plane = (int64_t)(g->ny + 2) * g->pitch;
+    k->zstride = (int64_t)g->q * k->plane;
+    return LBM_OK;
+}
+
+int check_params(const lbm_params_t* p, int q, KParams* k, cudaStream_t s, int real_bytes) {
+    if (!p) return fail(LBM_EINVAL, "params is NULL");
+    if (p->model < 0 || p->model > 2) return fail(LBM_EINVAL, "bad model %d", p->model);
+    if (p->force_mode < 0 || p->force_mode > 2)
+        return fail(LBM_EINVAL, "bad force mode %d", p->force_mode);
+    if (p->force_mode == LBM_FORCE_SHIFT && p->model != LBM_SRT)
+        return fail(LBM_EINVAL, "SimpleShift needs an SRT model with one global rate");
+    k->rem = p->rem;
+    k->hw = p->hw;
+    k->omega_e = p->omega_e;
+    k->omega_o = p->omega_o;
+    k->he_half = p->he_half;
+    k->ho_half = p->ho_half;
+    k->fx = p->fx;
+    k->fy = p->fy;
+    k->fz = p->fz;
+    k->sfx = p->shift_fx;
+    k->sfy = p->shift_fy;
+    k->sfz = p->shift_fz;
+    for (int i = 0; i < 27; ++i) {
+        k->ubb[i] = p->ubb[i];
+        k->pw[i] = p->pressure[i];
+    }
+    if (p->model == LBM_MRT) {
+        if (!p->mrt) return fail(LBM_EINVAL, "MRT needs its tables");
+        cudaError_t e = real_bytes == 8 ? set_mrt_tables_f64(q, p->mrt, s)
+                                        : set_mrt_tables_f32(q, p->mrt, s);
+        if (e != cudaSuccess) return cuda_status(e, "MRT tables");
+    }
+    return LBM_OK;
+}
+
+// ------------------------------------------------------------------ masks
+struct MaskBits {
+    uint32_t fluid, noslip, ubb, pressure, solid, known;
+};
+
+// neighbour flag source with the same covered/uncovered rule as pull_cell
+__device__ __forceinline__ uint32_t flag_at(const KGrid& g, const uint32_t* flags, int x, int y,
+                                            int z, int cx, int cy, int cz, bool* uncovered) {
+    const int X = g.nx + 2, Y = g.ny + 2;
+    int xs = x + cx, ys = y + cy, zs = z + cz;
+    bool unc = false;
+    int xw = xs, yw = ys, zw = zs;
+    if (xs < 0 || xs >= g.nx) {
+        if (g.wrap_x) xw = xs < 0 ? g.nx - 1 : 0;
+        else unc = true;
+    }
+    if (ys < 0 || ys >= g.ny) {
+        if (g.wrap_y) yw = ys < 0 ? g.ny - 1 : 0;
+        else unc = true;
+    }
+    if (zs < 0) {
+        if (g.zlo == LBM_ZFACE_WRAP) zw = g.nz - 1;
+        else if (g.zlo == LBM_ZFACE_GHOST) unc = true;
+    } else if (zs >= g.nz) {
+        if (g.zhi == LBM_ZFACE_WRAP) zw = 0;
+        else if (g.zhi == LBM_ZFACE_GHOST) unc = true;
+    }
+    if (unc) { xw = xs; yw = ys; zw = zs; }
+    *uncovered = unc;
+    return flags[((int64_t)(zw + 1) * Y + (yw + 1)) * X + (xw + 1)];
+}
+
+__device__ __forceinline__ void note_first(int* slot, int64_t cell) {
+    atomicMin(slot, (int)(cell + 1));
+}
+
+template <int Q>
+__global__ void k_build_mask(KGrid g, const uint32_t* __restrict__ flags, MaskBits b,
+                             uint32_t* __restrict__ cellmask, uint32_t* __restrict__ typemask,
+                             int* err) {
+    using D = Dirs<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    const int X = g.nx + 2, Y = g.ny + 2;
+    const uint32_t f = flags[((int64_t)(z + 1) * Y + (y + 1)) * X + (x + 1)];
+    const uint32_t flagged = f & b.known;
+    if (flagged & (flagged - 1u)) note_first(&err[0], cell);
+    if (flagged == 0u) note_first(&err[3], cell);
+    uint32_t code = 0, um = 0, pmk = 0;
+    int n_ubb = 0, n_ns = 0, n_pr = 0;
+    if (f & b.fluid) {
+        code = LBM_MASK_FLUID;
+        static_for<1, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            // pulled direction i reads x - c_i: the reference link (x, opp(i))
+            bool unc;
+            const uint32_t nb = flag_at(g, flags, x, y, z, -D::cx[i], -D::cy[i], -D::cz[i], &unc);
+            if (nb & b.solid) note_first(&err[1], cell);
+            if ((nb & b.known) == 0u) note_first(&err[2], cell);
+            if (unc && (nb & b.fluid)) note_first(&err[7], cell);
+            if (nb & b.noslip) { code |= 1u << i; ++n_ns; }
+            if (nb & b.ubb) { code |= 1u << i; um |= 1u << i; ++n_ubb; }
+            if (nb & b.pressure) { code |= 1u << i; pmk |= 1u << i; ++n_pr; }
+        });
+        if (um) code |= LBM_MASK_UBB;
+        if (pmk) code |= LBM_MASK_PRESSURE;
+    }
+    cellmask[cell] = code;
+    typemask[2 * cell] = um;
+    typemask[2 * cell + 1] = pmk;
+    if (n_ubb) atomicAdd(&err[4], n_ubb);
+    if (n_ns) atomicAdd(&err[5], n_ns);
+    if (n_pr) atomicAdd(&err[6], n_pr);
+}
+
+// ------------------------------------------------------------ flat cells
+template <int Q, int MODEL, int FORCE>
+__global__ void k_collide_cells(KParams p, double* __restrict__ f, int64_t n) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    double v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) v[i] = f[c * Q + i];
+    collide_cell<Q, MODEL, FORCE>(v, p);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[c * Q + i] = v[i];
+}
+
+template <int Q>
+__global__ void k_equilibrium_cells(const double* __restrict__ rho, const double* __restrict__ u,
+                                    double* __restrict__ f, int64_t n) {
+    using D = Dirs<Q>;
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const double r = rho[c];
+    const double ux = u[c * 3], uy = u[c * 3 + 1], uz = u[c * 3 + 2];
+    const double usq = (ux * ux + uy * uy) + uz * uz;
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        const double cu = cu_of<Q, i>(ux, uy, uz);
+        f[c * Q + i] = (wt<Q, i>() * r) * (((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq);
+    });
+}
+
+template <int Q, int GUO>
+__global__ void k_macroscopic_cells(KParams p, const double* __restrict__ f,
+                                    double* __restrict__ rho, double* __restrict__ u, int* bad,
+                                    int64_t n) {
+    using D = Dirs<Q>;
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    double v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) v[i] = f[c * Q + i];
+    double r = v[0];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) r = r + v[i];
+    if (r <= 0.0) atomicAdd(bad, 1);
+    double mx = 0.0, my = 0.0, mz = 0.0;
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        if constexpr (D::cx[i] == 1) mx = mx + v[i];
+        if constexpr (D::cx[i] == -1) mx = mx - v[i];
+        if constexpr (D::cy[i] == 1) my = my + v[i];
+        if constexpr (D::cy[i] == -1) my = my - v[i];
+        if constexpr (D::cz[i] == 1) mz = mz + v[i];
+        if constexpr (D::cz[i] == -1) mz = mz - v[i];
+    });
+    const double inv = 1.0 / r;
+    double ux = mx * inv, uy = my * inv, uz = mz * inv;
+    if constexpr (GUO) {
+        ux = ux + p.sfx * inv;
+        uy = uy + p.sfy * inv;
+        uz = uz + p.sfz * inv;
+    }
+    rho[c] = r;
+    u[c * 3] = ux;
+    u[c * 3 + 1] = uy;
+    u[c * 3 + 2] = uz;
+}
+
+template <class F>
+cudaError_t by_q(int q, F&& fn) {
+    if (q == 9) return fn(std::integral_constant<int, 9>{});
+    if (q == 19) return fn(std::integral_constant<int, 19>{});
+    if (q == 27) return fn(std::integral_constant<int, 27>{});
+    return cudaErrorInvalidValue;
+}
+
+dim3 cell_block(int nx) { return dim3(nx >= 128 ? 128 : ((nx + 31) / 32) * 32, 1, 1); }
+
+}  // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+int lbm_abi_version(void) { return LBM_B200_ABI_VERSION; }
+
+const char* lbm_last_error(void) { return g_err; }
+
+int lbm_slot_of(int q, int i) {
+    if (!q_ok(q) || i < 0 || i >= q) return -1;
+    if (q == 9) return slot_of<9>(i);
+    if (q == 19) return slot_of<19>(i);
+    return slot_of<27>(i);
+}
+
+int64_t lbm_field_elems(const lbm_grid_t* g) {
+    KGrid k;
+    if (check_grid(g, &k) != LBM_OK) return -1;
+    return (int64_t)(g->nz + 2) * k.zstride;
+}
+
+int lbm_face_span(const lbm_grid_t* g, int face, int64_t* send_off, int64_t* recv_off,
+                  int64_t* count) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (face != 0 && face != 1) return fail(LBM_EINVAL, "face must be 0 (low z) or 1 (high z)");
+    int nm, np;  // directions with c_z = -1, +1
+    if (g->q == 9) { nm = 0; np = 0; }
+    else if (g->q == 19) { nm = count_cz<19>(-1); np = count_cz<19>(1); }
+    else { nm = count_cz<27>(-1); np = count_cz<27>(1); }
+    if (face == 0) {
+        // receive into ghost plane z=-1 the directions pulled upward (c_z=+1);
+        // send interior plane z=0's c_z=-1 run (the lower peer's high ghost)
+        *recv_off = (int64_t)0 * k.zstride + (int64_t)(g->q - np) * k.plane;
+        *send_off = (int64_t)1 * k.zstride + 0;
+        *count = (int64_t)np * k.plane;
+        if (np != nm) return fail(LBM_EINVAL, "asymmetric stencil");
+    } else {
+        *recv_off = (int64_t)(g->nz + 1) * k.zstride + 0;
+        *send_off = (int64_t)g->nz * k.zstride + (int64_t)(g->q - np) * k.plane;
+        *count = (int64_t)nm * k.plane;
+    }
+    return LBM_OK;
+}
+
+int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p, const void* src, void* dst,
+                   const uint32_t* cellmask, const uint32_t* typemask, int z_begin, int z_end,
+                   void* stream) {
+    KGrid k;
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
+    if (!src || !dst || !cellmask || !typemask) return fail(LBM_EINVAL, "NULL buffer");
+    if (src == dst) return fail(LBM_EINVAL, "fused step needs two fields (src != dst)");
+    if (z_begin < 0 || z_end > g->nz || z_begin > z_end)
+        return fail(LBM_EINVAL, "plane range [%d, %d) outside 0..%d", z_begin, z_end, g->nz);
+    cudaError_t e = g->real_bytes == 8
+                        ? unit_f64::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
+                                          typemask, z_begin, z_end, s)
+                        : unit_f32::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
+                                          typemask, z_begin, z_end, s);
+    return cuda_status(e, "lbm_fused_step");
+}
+
+int lbm_collide_only(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,
+                     const uint32_t* cellmask, void* stream) {
+    KGrid k;
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
+    if (!pdf || !cellmask) return fail(LBM_EINVAL, "NULL buffer");
+    cudaError_t e = g->real_bytes == 8
+                        ? unit_f64::collide_only(g->q, p->model, p->force_mode, k, kp, pdf,
+                                                 cellmask, s)
+                        : unit_f32::collide_only(g->q, p->model, p->force_mode, k, kp, pdf,
+                                                 cellmask, s);
+    return cuda_status(e, "lbm_collide_only");
+}
+
+int lbm_stream_only(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
+                    const uint32_t* cellmask, const uint32_t* typemask, double* out,
+                    void* stream) {
+    KGrid k;
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
+    if (!src || !cellmask || !typemask || !out) return fail(LBM_EINVAL, "NULL buffer");
+    cudaError_t e = g->real_bytes == 8
+                        ? unit_f64::stream_only(g->q, k, kp, src, cellmask, typemask, out, s)
+                        : unit_f32::stream_only(g->q, k, kp, src, cellmask, typemask, out, s);
+    return cuda_status(e, "lbm_stream_only");
+}
+
+int lbm_moments(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
+                const uint32_t* cellmask, const uint32_t* typemask, int stream_form, double* rho,
+                double* u, int* bad_count, void* stream) {
+    KGrid k;
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
+    if (!src || !rho || !u || !bad_count) return fail(LBM_EINVAL, "NULL buffer");
+    if (stream_form && (!cellmask || !typemask)) return fail(LBM_EINVAL, "NULL mask");
+    const int guo = p->force_mode == LBM_FORCE_GUO;
+    cudaError_t e = g->real_bytes == 8 ? unit_f64::moments(g->q, guo, k, kp, src, cellmask, typemask,
+                                                           stream_form, rho, u, bad_count, s)
+                                       : unit_f32::moments(g->q, guo, k, kp, src, cellmask, typemask,
+                                                           stream_form, rho, u, bad_count, s);
+    return cuda_status(e, "lbm_moments");
+}
+
+int lbm_pack_rform(const lbm_grid_t* g, const double* dense, void* pdf, void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!dense || !pdf) return fail(LBM_EINVAL, "NULL buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = g->real_bytes == 8 ? unit_f64::convert(g->q, 1, k, (double*)dense, pdf, s)
+                                       : unit_f32::convert(g->q, 1, k, (double*)dense, pdf, s);
+    return cuda_status(e, "lbm_pack_rform");
+}
+
+int lbm_unpack_rform(const lbm_grid_t* g, const void* pdf, double* dense, void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!dense || !pdf) return fail(LBM_EINVAL, "NULL buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = g->real_bytes == 8 ? unit_f64::convert(g->q, 0, k, dense, (void*)pdf, s)
+                                       : unit_f32::convert(g->q, 0, k, dense, (void*)pdf, s);
+    return cuda_status(e, "lbm_unpack_rform");
+}
+
+int lbm_fill_equilibrium(const lbm_grid_t* g, const double* rho, const double* u, void* pdf,
+                         void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!rho || !u || !pdf) return fail(LBM_EINVAL, "NULL buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = g->real_bytes == 8 ? unit_f64::fill_eq(g->q, k, rho, u, pdf, s)
+                                       : unit_f32::fill_eq(g->q, k, rho, u, pdf, s);
+    return cuda_status(e, "lbm_fill_equilibrium");
+}
+
+int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags, const uint32_t bits[5],
+                       uint32_t* cellmask, uint32_t* typemask, int* err, void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!flags || !bits || !cellmask || !typemask || !err) return fail(LBM_EINVAL, "NULL buffer");
+    MaskBits b{bits[0], bits[1], bits[2], bits[3], bits[4], 0};
+    b.known = b.fluid | b.noslip | b.ubb | b.pressure | b.solid;
+    cudaStream_t s = (cudaStream_t)stream;
+    dim3 blk = cell_block(g->nx);
+    dim3 grid((g->nx + blk.x - 1) / blk.x, g->ny, g->nz);
+    cudaError_t e = by_q(g->q, [&](auto Qc) {
+        k_build_mask<decltype(Qc)::value><<<grid, blk, 0, s>>>(k, flags, b, cellmask, typemask, err);
+        return cudaGetLastError();
+    });
+    return cuda_status(e, "lbm_build_cellmask");
+}
+
+int lbm_collide_cells(int q, const lbm_params_t* p, double* f, int64_t n, void* stream) {
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!q_ok(q)) return fail(LBM_EINVAL, "q must be 9, 19 or 27, got %d", q);
+    if (!p) return fail(LBM_EINVAL, "params is NULL");
+    if (p->model == LBM_MRT) {
+        if (!p->mrt) return fail(LBM_EINVAL, "MRT needs its tables");
+        cudaError_t e = set_mrt_tables_capi(q, p->mrt, s);
+        if (e != cudaSuccess) return cuda_status(e, "MRT tables");
+    }
+    lbm_params_t copy = *p;
+    copy.model = p->model == LBM_MRT ? LBM_SRT : p->model;  // tables already set above
+    int st = check_params(&copy, q, &kp, s, 8);
+    if (st != LBM_OK) return st;
+    if (n <= 0) return LBM_OK;
+    if (!f) return fail(LBM_EINVAL, "NULL buffer");
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+    cudaError_t e = by_q(q, [&](auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        const int m = p->model, fm = p->force_mode;
+        if (m == 0 && fm == 0) k_collide_cells<Q, 0, 0><<<blocks, threads, 0, s>>>(kp, f, n);
+        else if (m == 0 && fm == 1) k_collide_cells<Q, 0, 1><<<blocks, threads, 0, s>>>(kp, f, n);
+        else if (m == 0 && fm == 2) k_collide_cells<Q, 0, 2><<<blocks, threads, 0, s>>>(kp, f, n);
+        else if (m == 1 && fm == 0) k_collide_cells<Q, 1, 0><<<blocks, threads, 0, s>>>(kp, f, n);
+        else if (m == 1 && fm == 1) k_collide_cells<Q, 1, 1><<<blocks, threads, 0, s>>>(kp, f, n);
+        else if (m == 2 && fm == 0) k_collide_cells<Q, 2, 0><<<blocks, threads, 0, s>>>(kp, f, n);
+        else if (m == 2 && fm == 1) k_collide_cells<Q, 2, 1><<<blocks, threads, 0, s>>>(kp, f, n);
+        else return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    });
+    return cuda_status(e, "lbm_collide_cells");
+}
+
+int lbm_equilibrium_cells(int q, const double* rho, const double* u, double* f, int64_t n,
+                          void* stream) {
+    if (!q_ok(q)) return fail(LBM_EINVAL, "q must be 9, 19 or 27, got %d", q);
+    if (n <= 0) return LBM_OK;
+    if (!rho || !u || !f) return fail(LBM_EINVAL, "NULL buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+    cudaError_t e = by_q(q, [&](auto Qc) {
+        k_equilibrium_cells<decltype(Qc)::value><<<blocks, threads, 0, s>>>(rho, u, f, n);
+        return cudaGetLastError();
+    });
+    return cuda_status(e, "lbm_equilibrium_cells");
+}
+
+int lbm_macroscopic_cells(int q, const lbm_params_t* p, const double* f, double* rho, double* u,
+                          int* bad_count, int64_t n, void* stream) {
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!q_ok(q)) return fail(LBM_EINVAL, "q must be 9, 19 or 27, got %d", q);
+    if (!p) return fail(LBM_EINVAL, "params is NULL");
+    lbm_params_t copy = *p;
+    copy.model = LBM_SRT;
+    if (copy.force_mode == LBM_FORCE_SHIFT) copy.force_mode = LBM_FORCE_NONE;
+    int st = check_params(&copy, q, &kp, s, 8);
+    if (st != LBM_OK) return st;
+    if (n <= 0) return LBM_OK;
+    if (!f || !rho || !u || !bad_count) return fail(LBM_EINVAL, "NULL buffer");
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+    const int guo = p->force_mode == LBM_FORCE_GUO;
+    cudaError_t e = by_q(q, [&](auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        if (guo) k_macroscopic_cells<Q, 1><<<blocks, threads, 0, s>>>(kp, f, rho, u, bad_count, n);
+        else k_macroscopic_cells<Q, 0><<<blocks, threads, 0, s>>>(kp, f, rho, u, bad_count, n);
+        return cudaGetLastError();
+    });
+    return cuda_status(e, "lbm_macroscopic_cells");
+}
+
+}  // extern "C"

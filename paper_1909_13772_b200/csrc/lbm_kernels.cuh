@@ -1,0 +1,344 @@
+// LBM sweep kernels for sm_100a (templated; instantiated in lbm_inst_*.cu).
+//
+// State on the device is the post-collision "G-form" G_n = C(R_n) where R_n is
+// the reference's stored state after n calls of stream_collide
+// (lbm/sweep.py:93-151: collide src in place -> stream_pull -> boundary
+// links -> swap).  One reference step R_{n+1} = S(C(R_n)) is re-bracketed as
+// G_{n+1} = C(S(G_n)): pull, bounce-back and collision of a cell happen in one
+// pass over HBM (2 q sizeof(real) bytes per cell + a 4-byte cell mask).
+//
+// Pull sources follow the reference's ghost semantics exactly:
+//   * a source inside the box is read directly;
+//   * a source on a periodic axis owned by this rank wraps (the reference's
+//     periodic self-exchange, field/ghost.py:112-124);
+//   * a source in a z ghost plane filled by the per-step exchange is read
+//     from that plane (x/y wrapped inside it like any interior plane);
+//   * a source outside the domain on a non-periodic axis ("uncovered") is
+//     the ghost cell itself at its raw index - the reference never writes
+//     those (exchange targets only images of the interior) so they keep the
+//     value written at fill time.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lbm_b200.h"
+#include "lbm_collide.cuh"
+
+namespace lbm {
+
+struct KGrid {
+    int nx, ny, nz, pitch, xoff;
+    int wrap_x, wrap_y, zlo, zhi;  // zlo/zhi: LBM_ZFACE_*
+    int64_t plane;                 // (ny+2) * pitch
+    int64_t zstride;               // q * plane
+};
+
+template <typename Real>
+struct Store;
+// fp64: stored as is
+template <>
+struct Store<double> {
+    template <int Q, int I>
+    __device__ __forceinline__ static double load(const double* p) { return __ldg(p); }
+    template <int Q, int I>
+    __device__ __forceinline__ static void store(double* p, double v) { *p = v; }
+};
+// fp32: stored zero-centred (f - w_i), arithmetic in fp64 registers
+template <>
+struct Store<float> {
+    template <int Q, int I>
+    __device__ __forceinline__ static double load(const float* p) {
+        return (double)__ldg(p) + wt<Q, I>();
+    }
+    template <int Q, int I>
+    __device__ __forceinline__ static void store(float* p, double v) {
+        *p = (float)(v - wt<Q, I>());
+    }
+};
+
+// per-axis source coordinate for a pull along -c (c in {-1,0,1})
+struct AxisSrc {
+    int lo_raw, hi_raw;    // coordinate - 1, coordinate + 1 (ghost-inclusive: may be -1 / n)
+    int lo_w, hi_w;        // wrapped (or raw when the axis does not wrap)
+    bool lo_unc, hi_unc;   // source outside the domain on a non-periodic axis
+};
+
+__device__ __forceinline__ AxisSrc make_axis(int c, int n, bool wrap, bool lo_unc_face,
+                                             bool hi_unc_face) {
+    AxisSrc a;
+    a.lo_raw = c - 1;
+    a.hi_raw = c + 1;
+    a.lo_w = (c == 0 && wrap) ? n - 1 : c - 1;
+    a.hi_w = (c == n - 1 && wrap) ? 0 : c + 1;
+    a.lo_unc = (c == 0) && lo_unc_face;
+    a.hi_unc = (c == n - 1) && hi_unc_face;
+    return a;
+}
+
+// element offset (relative to the field base) of (z, slot, y, x)
+__device__ __forceinline__ int64_t lidx(const KGrid& g, int z, int slot, int y, int x) {
+    return (int64_t)(z + 1) * g.zstride + (int64_t)slot * g.plane + (int64_t)(y + 1) * g.pitch +
+           g.xoff + x;
+}
+
+// Pressure anti-bounce-back for the pulled directions in `pm`
+// (boundary.py:171-195): rho, u from the cell's own post-collision state
+// (sequential sums, u = m / rho), then
+//   R[x, i] = -G[x, k] + (2 w_k rho_w) ((1 + (4.5 cu) cu) - 1.5 usq),  k = opp(i).
+template <int Q, typename Real>
+__device__ __noinline__ void pressure_links(const KGrid& g, const KParams& p,
+                                            const Real* __restrict__ src, int64_t own,
+                                            uint32_t pm, double (&f)[Q]) {
+    using D = Dirs<Q>;
+    double c[Q];
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        c[i] = Store<Real>::template load<Q, i>(src + own + (int64_t)slot_of<Q>(i) * g.plane);
+    });
+    double rho = c[0];
+#pragma unroll
+    for (int k = 1; k < Q; ++k) rho = rho + c[k];
+    double mx = 0.0, my = 0.0, mz = 0.0;
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        if constexpr (D::cx[i] == 1) mx = mx + c[i];
+        if constexpr (D::cx[i] == -1) mx = mx - c[i];
+        if constexpr (D::cy[i] == 1) my = my + c[i];
+        if constexpr (D::cy[i] == -1) my = my - c[i];
+        if constexpr (D::cz[i] == 1) mz = mz + c[i];
+        if constexpr (D::cz[i] == -1) mz = mz - c[i];
+    });
+    const double ux = mx / rho, uy = my / rho, uz = mz / rho;
+    const double usq15 = 1.5 * ((ux * ux + uy * uy) + uz * uz);
+    static_for<1, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        constexpr int k = D::opp[i];
+        if ((pm >> i) & 1u) {
+            const double cu = cu_of<Q, k>(ux, uy, uz);
+            f[i] = -c[k] + p.pw[k] * ((1.0 + (4.5 * cu) * cu) - usq15);
+        }
+    });
+}
+
+// Load the 19/27/9 pulled populations of cell (x,y,z) with the fused
+// bounce-back substitution R[x,i] = G[x,opp(i)] (- UBB term) for masked
+// directions (boundary.py:163-170).
+template <int Q, typename Real>
+__device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
+                                          const Real* __restrict__ src, int x, int y, int z,
+                                          uint32_t code, const uint32_t* __restrict__ typemask,
+                                          bool generic, double (&f)[Q]) {
+    using D = Dirs<Q>;
+    const int64_t own = lidx(g, z, 0, y, x);
+    uint32_t tm = 0, pm = 0;
+    if (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) {
+        const uint2 t = *reinterpret_cast<const uint2*>(typemask + 2 * (((int64_t)z * g.ny + y) * g.nx + x));
+        tm = t.x;
+        pm = t.y;
+    }
+    AxisSrc ax, ay, az;
+    if (generic) {
+        ax = make_axis(x, g.nx, g.wrap_x, !g.wrap_x, !g.wrap_x);
+        ay = make_axis(y, g.ny, g.wrap_y, !g.wrap_y, !g.wrap_y);
+        az = make_axis(z, g.nz, false, g.zlo == LBM_ZFACE_GHOST, g.zhi == LBM_ZFACE_GHOST);
+        if (g.zlo == LBM_ZFACE_WRAP && z == 0) az.lo_w = g.nz - 1;
+        if (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1) az.hi_w = 0;
+    }
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        constexpr int cx = D::cx[i], cy = D::cy[i], cz = D::cz[i];
+        constexpr int so = slot_of<Q>(i);
+        int64_t off;
+        if (!generic) {
+            off = own + (int64_t)so * g.plane - (int64_t)cz * g.zstride - (int64_t)cy * g.pitch - cx;
+        } else {
+            bool unc = false;
+            int xs = x, ys = y, zs = z, xr = x, yr = y, zr = z;
+            if constexpr (cx == 1) { xs = ax.lo_w; xr = ax.lo_raw; unc |= ax.lo_unc; }
+            if constexpr (cx == -1) { xs = ax.hi_w; xr = ax.hi_raw; unc |= ax.hi_unc; }
+            if constexpr (cy == 1) { ys = ay.lo_w; yr = ay.lo_raw; unc |= ay.lo_unc; }
+            if constexpr (cy == -1) { ys = ay.hi_w; yr = ay.hi_raw; unc |= ay.hi_unc; }
+            if constexpr (cz == 1) { zs = az.lo_w; zr = az.lo_raw; unc |= az.lo_unc; }
+            if constexpr (cz == -1) { zs = az.hi_w; zr = az.hi_raw; unc |= az.hi_unc; }
+            if (unc) { xs = xr; ys = yr; zs = zr; }
+            off = lidx(g, zs, so, ys, xs);
+        }
+        if constexpr (i != 0) {
+            // link: read the own cell's direction k = opp(i) instead (w_k == w_i,
+            // so the fp32 zero-centring offset is the same)
+            constexpr int k = D::opp[i];
+            const bool link = (code >> i) & 1u;
+            if (link) off = own + (int64_t)slot_of<Q>(k) * g.plane;
+            double v = Store<Real>::template load<Q, i>(src + off);
+            if ((tm >> i) & 1u) v = v - p.ubb[k];
+            f[i] = v;
+        } else {
+            f[0] = Store<Real>::template load<Q, 0>(src + off);
+        }
+    });
+    if (pm) pressure_links<Q, Real>(g, p, src, own, pm, f);
+}
+
+// Fused pull -> bounce-back -> collide over interior planes [z0, z0+gridDim.z).
+template <int Q, typename Real, int MODEL, int FORCE>
+__global__ void __launch_bounds__(128) k_fused(KGrid g, KParams p, const Real* __restrict__ src,
+                                               Real* __restrict__ dst,
+                                               const uint32_t* __restrict__ cellmask,
+                                               const uint32_t* __restrict__ typemask, int z0) {
+    using D = Dirs<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = z0 + blockIdx.z;
+    // warp-uniform choice of the index path: wrapping only near periodic edges
+    const int xw0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    const bool edge_x = g.wrap_x && (xw0 == 0 || xw0 + 32 >= g.nx);
+    const bool edge_y = g.wrap_y && (y == 0 || y == g.ny - 1);
+    const bool edge_z = (g.zlo == LBM_ZFACE_WRAP && z == 0) || (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1);
+    const bool generic = edge_x || edge_y || edge_z;
+    if (x >= g.nx) return;
+    const uint32_t code = __ldg(cellmask + ((int64_t)z * g.ny + y) * g.nx + x);
+    double f[Q];
+    pull_cell<Q, Real>(g, p, src, x, y, z, code, typemask, generic, f);
+    if (code & LBM_MASK_FLUID) collide_cell<Q, MODEL, FORCE>(f, p);
+    const int64_t own = lidx(g, z, 0, y, x);
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        Store<Real>::template store<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
+    });
+}
+
+// G_0 = C(R_0): collide fluid interior cells in place.
+template <int Q, typename Real, int MODEL, int FORCE>
+__global__ void __launch_bounds__(128) k_collide_only(KGrid g, KParams p, Real* __restrict__ pdf,
+                                                      const uint32_t* __restrict__ cellmask) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const uint32_t code = cellmask[((int64_t)z * g.ny + y) * g.nx + x];
+    if (!(code & LBM_MASK_FLUID)) return;
+    const int64_t own = lidx(g, z, 0, y, x);
+    double f[Q];
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        f[i] = Store<Real>::template load<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane);
+    });
+    collide_cell<Q, MODEL, FORCE>(f, p);
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        Store<Real>::template store<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
+    });
+}
+
+// R = S(G) to dense fp64 (q, nz, ny, nx), reference direction order.
+template <int Q, typename Real>
+__global__ void __launch_bounds__(128) k_stream_only(KGrid g, KParams p, const Real* __restrict__ src,
+                                                     const uint32_t* __restrict__ cellmask,
+                                                     const uint32_t* __restrict__ typemask,
+                                                     double* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    const uint32_t code = cellmask[cell];
+    double f[Q];
+    pull_cell<Q, Real>(g, p, src, x, y, z, code, typemask, true, f);
+    const int64_t n = (int64_t)g.nx * g.ny * g.nz;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) out[(int64_t)i * n + cell] = f[i];
+}
+
+// rho/u (collision.py:167-184) of R = S(G) (stream_form) or of the stored R.
+template <int Q, typename Real, int GUO>
+__global__ void __launch_bounds__(128) k_moments(KGrid g, KParams p, const Real* __restrict__ src,
+                                                 const uint32_t* __restrict__ cellmask,
+                                                 const uint32_t* __restrict__ typemask,
+                                                 int stream_form, double* __restrict__ rho_out,
+                                                 double* __restrict__ u_out, int* bad) {
+    using D = Dirs<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    double f[Q];
+    if (stream_form) {
+        pull_cell<Q, Real>(g, p, src, x, y, z, cellmask[cell], typemask, true, f);
+    } else {
+        const int64_t own = lidx(g, z, 0, y, x);
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            f[i] = Store<Real>::template load<Q, i>(src + own + (int64_t)slot_of<Q>(i) * g.plane);
+        });
+    }
+    double rho = f[0];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) rho = rho + f[i];
+    if (rho <= 0.0) atomicAdd(bad, 1);
+    double mx = 0.0, my = 0.0, mz = 0.0;
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        if constexpr (D::cx[i] == 1) mx = mx + f[i];
+        if constexpr (D::cx[i] == -1) mx = mx - f[i];
+        if constexpr (D::cy[i] == 1) my = my + f[i];
+        if constexpr (D::cy[i] == -1) my = my - f[i];
+        if constexpr (D::cz[i] == 1) mz = mz + f[i];
+        if constexpr (D::cz[i] == -1) mz = mz - f[i];
+    });
+    const double inv = 1.0 / rho;
+    double ux = mx * inv, uy = my * inv, uz = mz * inv;
+    if constexpr (GUO) {
+        ux = ux + p.sfx * inv;
+        uy = uy + p.sfy * inv;
+        uz = uz + p.sfz * inv;
+    }
+    rho_out[cell] = rho;
+    u_out[cell * 3 + 0] = ux;
+    u_out[cell * 3 + 1] = uy;
+    u_out[cell * 3 + 2] = uz;
+}
+
+// dense ghost-inclusive (q, Z, Y, X) fp64 <-> layout
+template <int Q, typename Real, int TO_LAYOUT>
+__global__ void k_convert(KGrid g, double* __restrict__ dense, Real* __restrict__ pdf) {
+    const int X = g.nx + 2, Y = g.ny + 2, Z = g.nz + 2;
+    const int xg = blockIdx.x * blockDim.x + threadIdx.x;
+    const int yg = blockIdx.y;
+    const int zg = blockIdx.z;
+    if (xg >= X) return;
+    const int64_t n = (int64_t)X * Y * Z;
+    const int64_t cell = ((int64_t)zg * Y + yg) * X + xg;
+    const int64_t own = lidx(g, zg - 1, 0, yg - 1, xg - 1);
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        Real* pp = pdf + own + (int64_t)slot_of<Q>(i) * g.plane;
+        if constexpr (TO_LAYOUT) Store<Real>::template store<Q, i>(pp, dense[i * n + cell]);
+        else dense[i * n + cell] = Store<Real>::template load<Q, i>(pp);
+    });
+}
+
+// equilibrium() (collision.py:150-154) into the layout, ghosts included
+template <int Q, typename Real>
+__global__ void k_fill_eq(KGrid g, const double* __restrict__ rho, const double* __restrict__ u,
+                          Real* __restrict__ pdf) {
+    using D = Dirs<Q>;
+    const int X = g.nx + 2, Y = g.ny + 2;
+    const int xg = blockIdx.x * blockDim.x + threadIdx.x;
+    const int yg = blockIdx.y;
+    const int zg = blockIdx.z;
+    if (xg >= X) return;
+    const int64_t cell = ((int64_t)zg * Y + yg) * X + xg;
+    const double r = rho[cell];
+    const double ux = u[cell * 3], uy = u[cell * 3 + 1], uz = u[cell * 3 + 2];
+    const double usq = (ux * ux + uy * uy) + uz * uz;
+    const int64_t own = lidx(g, zg - 1, 0, yg - 1, xg - 1);
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        const double cu = cu_of<Q, i>(ux, uy, uz);
+        const double feq = (wt<Q, i>() * r) * (((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq);
+        Store<Real>::template store<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane, feq);
+    });
+}
+
+}  // namespace lbm

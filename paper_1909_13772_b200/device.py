@@ -1,0 +1,408 @@
+"""HBM-resident lattice state behind a PdfField.
+
+`RankBox` maps this rank's blocks onto one contiguous device box (a z-slab
+when several ranks share the domain).  `DeviceLattice`
+owns the two PDF buffers in the z-q-y-x layout of include/lbm_b200.h and runs
+the per-step schedule:
+
+* state is the post-collision G-form G_n = C(R_n); the reference state R_n
+  (what `pdf.src(block)` holds after n sweeps, lbm/sweep.py:93-151) is
+  recovered on demand as S(G_{n-1}) from the swapped-out buffer;
+* P = 1: one fused launch per step (periodic z wraps in the kernel);
+* P > 1: boundary planes first on a high-priority stream, their crossing
+  directions sent zero-copy to the z-neighbours (NCCL send/recv straight
+  from / into the field), the interior planes computed concurrently on the
+  caller's stream.
+
+Host<->device traffic happens only on upload (host R-form written by the
+user), readout (host arrays touched) and mask builds; never inside the step.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import BackendError, ValidationError
+
+
+def _round_up(v, m):
+    return (v + m - 1) // m * m
+
+
+class RankBox:
+    """This rank's blocks as one box in global cell coordinates."""
+
+    def __init__(self, forest):
+        if forest.cells_per_block is None:
+            raise ValidationError("forest has no cells_per_block")
+        ctx = forest.ctx
+        blocks = forest.local_blocks()
+        if not blocks:
+            raise ValidationError(f"rank {ctx.rank} owns no block; use at least as many "
+                                  "blocks as ranks")
+        boxes = [forest.cell_box(b.id) for b in blocks]
+        lo = tuple(min(b[0][a] for b in boxes) for a in range(3))
+        hi = tuple(max(b[1][a] for b in boxes) for a in range(3))
+        vol = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2])
+        if vol != sum((b[1][0] - b[0][0]) * (b[1][1] - b[0][1]) * (b[1][2] - b[0][2]) for b in boxes):
+            raise ValidationError("the blocks of a rank must form one box on the B200 path "
+                                  "(use root_dims = (1, 1, P) z-slabs)")
+        N = forest.global_cells(0)
+        self.global_cells = N
+        if ctx.n_ranks > 1 and (lo[0] != 0 or lo[1] != 0 or hi[0] != N[0] or hi[1] != N[1]):
+            raise ValidationError("multi-rank B200 runs partition the domain in z-slabs: every "
+                                  "rank's box must span the full x and y extent")
+        self.lo, self.hi = lo, hi
+        self.nx, self.ny, self.nz = (hi[a] - lo[a] for a in range(3))
+        self.blocks = blocks
+        self.offsets = [tuple(b[0][a] - lo[a] for a in range(3)) for b in boxes]
+        per = forest.periodic
+        self.wrap_x = bool(per[0]) and lo[0] == 0 and hi[0] == N[0]
+        self.wrap_y = bool(per[1]) and lo[1] == 0 and hi[1] == N[1]
+        if (per[0] and not self.wrap_x) or (per[1] and not self.wrap_y):
+            raise ValidationError("periodic x/y must be owned by one rank (z-slab partition)")
+        self.lo_peer = self.hi_peer = None
+        # low z face
+        if lo[2] > 0:
+            self.zface_lo, self.lo_peer = _lib.ZFACE_HALO, forest.owner_of_cell((0, 0, lo[2] - 1))
+        elif per[2]:
+            peer = forest.owner_of_cell((0, 0, N[2] - 1))
+            if peer == ctx.rank:
+                self.zface_lo = _lib.ZFACE_WRAP
+            else:
+                self.zface_lo, self.lo_peer = _lib.ZFACE_HALO, peer
+        else:
+            self.zface_lo = _lib.ZFACE_GHOST
+        # high z face
+        if hi[2] < N[2]:
+            self.zface_hi, self.hi_peer = _lib.ZFACE_HALO, forest.owner_of_cell((0, 0, hi[2]))
+        elif per[2]:
+            peer = forest.owner_of_cell((0, 0, 0))
+            if peer == ctx.rank:
+                self.zface_hi = _lib.ZFACE_WRAP
+            else:
+                self.zface_hi, self.hi_peer = _lib.ZFACE_HALO, peer
+        else:
+            self.zface_hi = _lib.ZFACE_GHOST
+        if (self.zface_lo == _lib.ZFACE_WRAP) != (self.zface_hi == _lib.ZFACE_WRAP):
+            raise ValidationError("periodic z wrap must be owned entirely by one rank")
+
+    @property
+    def cells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    # ------------------------------------------------- host box assembly
+    def gather(self, views, nf, dtype):
+        """Ghost-inclusive box (nf, Z, Y, X) from per-block logical views
+        (z, y, x, f) with one ghost layer: block ghost layers first (they
+        provide the box's outer ghost shell), then every interior."""
+        out = np.zeros((nf, self.nz + 2, self.ny + 2, self.nx + 2), dtype=dtype)
+        for v, (ox, oy, oz) in zip(views, self.offsets):
+            sub = out[:, oz:oz + v.shape[0], oy:oy + v.shape[1], ox:ox + v.shape[2]]
+            sub[...] = np.moveaxis(v, 3, 0)
+        for v, (ox, oy, oz) in zip(views, self.offsets):
+            n0, n1, n2 = v.shape[0] - 2, v.shape[1] - 2, v.shape[2] - 2
+            out[:, 1 + oz:1 + oz + n0, 1 + oy:1 + oy + n1, 1 + ox:1 + ox + n2] = \
+                np.moveaxis(v[1:-1, 1:-1, 1:-1], 3, 0)
+        return out
+
+    def scatter_interior(self, dense, views):
+        """dense (nf, nz, ny, nx) -> block interiors of logical views."""
+        for v, (ox, oy, oz) in zip(views, self.offsets):
+            n0, n1, n2 = v.shape[0] - 2, v.shape[1] - 2, v.shape[2] - 2
+            v[1:-1, 1:-1, 1:-1] = np.moveaxis(dense[:, oz:oz + n0, oy:oy + n1, ox:ox + n2], 0, 3)
+
+    def scatter_full(self, dense_g, views):
+        """dense ghost-inclusive (nf, Z, Y, X) -> block views incl. ghosts."""
+        for v, (ox, oy, oz) in zip(views, self.offsets):
+            v[...] = np.moveaxis(dense_g[:, oz:oz + v.shape[0], oy:oy + v.shape[1],
+                                         ox:ox + v.shape[2]], 0, 3)
+
+
+class Masks:
+    """Device cell mask + link-type mask for one (box, stencil, flags) state."""
+
+    def __init__(self, cellmask, typemask, counts, unflagged_cell=None):
+        self.cellmask = cellmask      # int32 (nz, ny, nx)
+        self.typemask = typemask      # int32 (nz, ny, nx, 2)
+        self.counts = counts          # dict NoSlip/UBB/Pressure -> links on this rank
+        self.unflagged_cell = unflagged_cell
+
+
+def all_fluid_masks(box: RankBox, device) -> Masks:
+    cm = torch.full((box.nz, box.ny, box.nx), _lib.MASK_FLUID, dtype=torch.int32, device=device)
+    tm = torch.zeros((box.nz, box.ny, box.nx, 2), dtype=torch.int32, device=device)
+    return Masks(cm, tm, {"NoSlip": 0, "UBB": 0, "Pressure": 0})
+
+
+class DeviceLattice:
+    """Two HBM PDF buffers plus the step schedule for one PdfField."""
+
+    def __init__(self, pdf, dtype="float64"):
+        forest = pdf.forest
+        self.pdf = pdf
+        self.forest = forest
+        self.ctx = forest.ctx
+        self.q = pdf.stencil.q
+        if dtype not in ("float64", "float32"):
+            raise ValidationError(f"PDF dtype must be float64 or float32, got {dtype!r}")
+        self.real_bytes = 8 if dtype == "float64" else 4
+        self.tdtype = torch.float64 if dtype == "float64" else torch.float32
+        if not torch.cuda.is_available():
+            raise BackendError("no CUDA device: the B200 path has no CPU fallback")
+        _lib.load()
+        self.device = self.ctx.device if self.ctx.device.type == "cuda" else torch.device("cuda")
+        self.box = box = RankBox(forest)
+        elems_line = 128 // self.real_bytes
+        g = _lib.Grid()
+        g.q, g.real_bytes = self.q, self.real_bytes
+        g.nx, g.ny, g.nz = box.nx, box.ny, box.nz
+        g.xoff = elems_line
+        g.pitch = _round_up(elems_line + box.nx + 1, elems_line)
+        g.wrap_x, g.wrap_y = int(box.wrap_x), int(box.wrap_y)
+        g.zface_lo, g.zface_hi = box.zface_lo, box.zface_hi
+        self.grid = g
+        self.gref = ctypes.byref(g)
+        self.elems = int(_lib.load().lbm_field_elems(self.gref))
+        if self.elems <= 0:
+            _lib.call("lbm_field_elems", self.gref)
+        self.buf = [torch.empty(self.elems, dtype=self.tdtype, device=self.device),
+                    torch.empty(self.elems, dtype=self.tdtype, device=self.device)]
+        self.cur = 0
+        self.cur_kind = None      # None / "R" / "G"
+        self.prev_kind = None     # None / "R" / "G"
+        self.coll_key = None      # (params key, masks) that produced the current G
+        self.stream_masks = None  # masks used by the pull that produced R_n
+        self.host_state = "host"  # "host": host authoritative; "device": host stale; "synced"
+        self.snapshot = None
+        self.steps = 0
+        self._halo = None
+        self._streams = None
+        self._fluid_masks = None
+
+    # ---------------------------------------------------------- plumbing
+    @property
+    def stream(self):
+        return torch.cuda.current_stream(self.device)
+
+    def _sp(self, stream=None):
+        return _lib.stream_ptr(stream if stream is not None else self.stream)
+
+    def default_masks(self) -> Masks:
+        if self._fluid_masks is None:
+            self._fluid_masks = all_fluid_masks(self.box, self.device)
+        return self._fluid_masks
+
+    def _views(self, key):
+        return [b.data[key].view_nosync for b in self.box.blocks]
+
+    # ------------------------------------------------------ host <-> HBM
+    def upload_host(self):
+        """Host R-form (src slot, ghosts incl.) -> buffer[cur] (kind R)."""
+        dense = self.box.gather(self._views(self.pdf.key), self.q, np.float64)
+        t = torch.from_numpy(dense).pin_memory().to(self.device, non_blocking=True)
+        _lib.call("lbm_pack_rform", self.gref, _lib.ptr(t), _lib.ptr(self.buf[self.cur]), self._sp())
+        self.cur_kind, self.prev_kind = "R", None
+        self.coll_key = None
+        self.host_state = "synced"
+        self.snapshot = None
+        self.halo_sync_rform()
+        torch.cuda.current_stream(self.device).synchronize()
+        del t
+
+    def fill_equilibrium(self, rho_g, u_g):
+        """rho (Z,Y,X), u (Z,Y,X,3) ghost-inclusive box -> buffer[cur] (kind R)."""
+        tr = torch.from_numpy(np.ascontiguousarray(rho_g, dtype=np.float64)).to(self.device)
+        tu = torch.from_numpy(np.ascontiguousarray(u_g, dtype=np.float64)).to(self.device)
+        _lib.call("lbm_fill_equilibrium", self.gref, _lib.ptr(tr), _lib.ptr(tu),
+                  _lib.ptr(self.buf[self.cur]), self._sp())
+        self.cur_kind, self.prev_kind = "R", None
+        self.coll_key = None
+        self.host_state = "device"
+        self.snapshot = None
+
+    def halo_sync_rform(self):
+        """R-form halos are not needed: G_0 = C(R_0) is computed on the
+        interior and its crossing directions exchanged afterwards."""
+
+    def readout_device(self):
+        """R_n on the device: ("full", (q,Z,Y,X)) when a raw R-form is held,
+        else ("interior", (q,nz,ny,nx)) = S(G_{n-1}) by the stream-only kernel."""
+        self.join_streams()
+        b = self.box
+        if self.cur_kind == "R" or self.prev_kind == "R":
+            src = self.buf[self.cur] if self.cur_kind == "R" else self.buf[1 - self.cur]
+            out = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
+                              device=self.device)
+            _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(src), _lib.ptr(out), self._sp())
+            return "full", out
+        if self.cur_kind is None:
+            raise ValidationError("PDF field has no device state")
+        m = self.stream_masks
+        out = torch.empty((self.q, b.nz, b.ny, b.nx), dtype=torch.float64, device=self.device)
+        _lib.call("lbm_stream_only", self.gref, self._kp_stream.ref,
+                  _lib.ptr(self.buf[1 - self.cur]), _lib.ptr(m.cellmask), _lib.ptr(m.typemask),
+                  _lib.ptr(out), self._sp())
+        return "interior", out
+
+    def readout(self):
+        kind, t = self.readout_device()
+        return kind, t.cpu().numpy()
+
+    def sync_host(self):
+        """Pull R_n into the host block arrays of the src slot (idempotent)."""
+        if self.host_state != "device":
+            return
+        kind, dense = self.readout()
+        views = self._views(self.pdf.key)
+        if kind == "full":
+            self.box.scatter_full(dense, views)
+        else:
+            self.box.scatter_interior(dense, views)
+        self.host_state = "synced"
+        self.snapshot = None
+
+    def host_touched(self):
+        """Called when host arrays are handed out while synced: remember the
+        content so the next sweep can tell whether the user wrote into it."""
+        if self.host_state == "synced" and self.snapshot is None:
+            self.snapshot = [v.copy() for v in self._views(self.pdf.key)]
+
+    def host_changed(self) -> bool:
+        if self.host_state == "host":
+            return True
+        if self.host_state == "device" or self.snapshot is None:
+            return False
+        return any(not np.array_equal(a, b) for a, b in zip(self.snapshot, self._views(self.pdf.key)))
+
+    # ------------------------------------------------------------ steps
+    def _streams_get(self):
+        if self._streams is None:
+            lo, hi = torch.cuda.Stream.priority_range()
+            self._streams = {"boundary": torch.cuda.Stream(self.device, priority=hi),
+                             "ev_b": torch.cuda.Event(), "ev_i": torch.cuda.Event(),
+                             "pending": False}
+        return self._streams
+
+    def join_streams(self):
+        """Make the caller's stream wait for any boundary/halo work."""
+        if self._streams is not None and self._streams["pending"]:
+            self.stream.wait_stream(self._streams["boundary"])
+            self._streams["pending"] = False
+
+    @property
+    def halo(self):
+        if self._halo is None:
+            from .halo import Halo
+            self._halo = Halo(self)
+        return self._halo
+
+    def ensure_collided(self, kp, key, masks):
+        """Make buffer[cur] hold G_n = C_key(R_n)."""
+        if self.cur_kind == "G" and self.coll_key == key:
+            return
+        self.join_streams()
+        if self.cur_kind == "G":
+            # model / flags changed between sweeps: the stored G_n was collided
+            # with the old key.  Rebuild R_n = S(G_{n-1}) (old pull masks) into
+            # buffer[cur] - its ghost shell stays valid - and collide again.
+            kind, inner = self.readout_device()
+            b = self.box
+            full = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
+                               device=self.device)
+            _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(self.buf[self.cur]),
+                      _lib.ptr(full), self._sp())
+            full[:, 1:-1, 1:-1, 1:-1] = inner
+            _lib.call("lbm_pack_rform", self.gref, _lib.ptr(full), _lib.ptr(self.buf[self.cur]),
+                      self._sp())
+            self.cur_kind = "R"
+        if self.cur_kind != "R":
+            raise ValidationError("PDF field has no device state")
+        # keep R_n in the other buffer (step-0 readouts, ghost shell of both)
+        self.buf[1 - self.cur].copy_(self.buf[self.cur])
+        self.prev_kind = "R"
+        _lib.call("lbm_collide_only", self.gref, kp.ref, _lib.ptr(self.buf[self.cur]),
+                  _lib.ptr(masks.cellmask), self._sp())
+        if self.has_halo:
+            self.halo.exchange(self.buf[self.cur], self.stream)
+        self.cur_kind = "G"
+        self.coll_key = key
+
+    @property
+    def has_halo(self) -> bool:
+        return self.box.zface_lo == _lib.ZFACE_HALO or self.box.zface_hi == _lib.ZFACE_HALO
+
+    def step(self, kp, key, masks, nsteps=1):
+        """nsteps fused sweeps G_{n+1} = C(S(G_n))."""
+        self.ensure_collided(kp, key, masks)
+        nz = self.box.nz
+        cm, tm = _lib.ptr(masks.cellmask), _lib.ptr(masks.typemask)
+        lib = _lib.load()
+        main = self.stream
+        if self.has_halo:
+            S = self._streams_get()
+            S["boundary"].wait_stream(main)
+        for n in range(nsteps):
+            src, dst = self.buf[self.cur], self.buf[1 - self.cur]
+            if not self.has_halo:
+                st = lib.lbm_fused_step(self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
+                                        0, nz, self._sp(main))
+                if st:
+                    _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst),
+                              cm, tm, 0, nz, self._sp(main))
+            else:
+                self._halo_step(kp, src, dst, cm, tm, main, first=(n == 0))
+            self.cur = 1 - self.cur
+            self.prev_kind = "G"
+            self.steps += 1
+        self.stream_masks = masks
+        self._kp_stream = kp
+        self.host_state = "device"
+        self.snapshot = None
+
+    def _halo_step(self, kp, src, dst, cm, tm, main, first):
+        """One overlapped step: B(n) = boundary planes on the high-priority
+        stream followed by the zero-copy halo send/recv, I(n) = interior
+        planes on the caller's stream.  Hazards: B(n) after I(n-1) (B writes
+        planes I(n-1) reads); I(n) after B(n-1) (I writes planes B(n-1)
+        reads); B(n+1) after the halo of step n (stream order)."""
+        S = self._streams_get()
+        sb = S["boundary"]
+        nz = self.box.nz
+        if not first:
+            main.wait_event(S["ev_b"])       # I(n) after B(n-1)
+            sb.wait_event(S["ev_i"])         # B(n) after I(n-1)
+        for z in sorted({0, nz - 1}):
+            _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
+                      z, z + 1, self._sp(sb))
+        S["ev_b"].record(sb)
+        self.halo.exchange(dst, sb)
+        if nz > 2:
+            _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
+                      1, nz - 1, self._sp(main))
+        S["ev_i"].record(main)
+        S["pending"] = True
+
+    # ---------------------------------------------------------- readout
+    def moments(self, kp, masks):
+        """rho (nz,ny,nx), u (nz,ny,nx,3) of R_n on the host, fp64."""
+        self.join_streams()
+        b = self.box
+        rho = torch.empty((b.nz, b.ny, b.nx), dtype=torch.float64, device=self.device)
+        u = torch.empty((b.nz, b.ny, b.nx, 3), dtype=torch.float64, device=self.device)
+        bad = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if self.cur_kind == "R":
+            _lib.call("lbm_moments", self.gref, kp.ref, _lib.ptr(self.buf[self.cur]), None, None, 0,
+                      _lib.ptr(rho), _lib.ptr(u), _lib.ptr(bad), self._sp())
+        elif self.prev_kind == "R":
+            _lib.call("lbm_moments", self.gref, kp.ref, _lib.ptr(self.buf[1 - self.cur]), None, None,
+                      0, _lib.ptr(rho), _lib.ptr(u), _lib.ptr(bad), self._sp())
+        else:
+            m = self.stream_masks
+            _lib.call("lbm_moments", self.gref, kp.ref, _lib.ptr(self.buf[1 - self.cur]),
+                      _lib.ptr(m.cellmask), _lib.ptr(m.typemask), 1, _lib.ptr(rho), _lib.ptr(u),
+                      _lib.ptr(bad), self._sp())
+        return rho, u, bad

@@ -1,0 +1,222 @@
+"""Flag-driven boundary conditions: registry, validation, device link masks.
+
+Same flags, registry order and validation rules as the reference
+(pkg/src/blocksim/lbm/boundary.py:26-195).  Instead of per-type link lists
+scattered after the stream (BoundaryHandling.apply), `freeze()` builds a
+per-cell link mask on the device (lbm_build_cellmask) that the fused
+stream-collide kernel consumes, so bounce-back costs 4 bytes per cell inside
+the one pass over HBM.  `links` / `build_index_lists` decode that mask back
+into the reference's list format for inspection and tests.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from .. import _lib
+from ..device import Masks, RankBox
+from ..errors import ValidationError
+from ..field import FlagFieldHandler, GhostPackInfo, exchange_ghosts
+from .stencil import Stencil
+
+FLUID = "Fluid"
+NO_SLIP = "NoSlip"
+UBB = "UBB"
+PRESSURE = "Pressure"
+SOLID = "Solid"
+BOUNDARY_FLAGS = (FLUID, NO_SLIP, UBB, PRESSURE, SOLID)
+_LINK_FLAGS = (NO_SLIP, UBB, PRESSURE)
+
+
+def ensure_flags(forest, flags="flags", ghost_layers=1) -> FlagFieldHandler:
+    """Register the flag slot if needed and the canonical flag names
+    (boundary.py:35-45)."""
+    if flags not in forest.handlers:
+        forest.register_data(flags, FlagFieldHandler(ghost_layers))
+    handler = forest.handlers[flags]
+    if not isinstance(handler, FlagFieldHandler):
+        raise ValidationError(f"data slot {flags!r} is not a flag field")
+    for name in BOUNDARY_FLAGS:
+        if name not in handler.registry:
+            handler.register(name)
+    return handler
+
+
+def _flag_bits(registry):
+    return (ctypes.c_uint32 * 5)(*(int(registry[n]) for n in (FLUID, NO_SLIP, UBB, PRESSURE, SOLID)))
+
+
+def build_masks(forest, stencil: Stencil, flags="flags", device=None) -> Masks:
+    """Device link masks of this rank's box from the host flags (ghost
+    flags must be current).  Raises the reference's ValidationErrors."""
+    import torch
+    box = RankBox(forest)
+    blocks = box.blocks
+    for b in blocks:
+        if b.data[flags].g < 1:
+            raise ValidationError("boundary links need one flag ghost layer")
+    views = [b.data[flags].field.view_nosync for b in blocks]
+    dense = box.gather(views, 1, np.uint32)[0]
+    if device is None:
+        device = forest.ctx.device if forest.ctx.device.type == "cuda" else torch.device("cuda")
+    g = _lib.Grid()
+    g.q, g.real_bytes = stencil.q, 8
+    g.nx, g.ny, g.nz = box.nx, box.ny, box.nz
+    g.xoff, g.pitch = 1, box.nx + 2
+    g.wrap_x, g.wrap_y = int(box.wrap_x), int(box.wrap_y)
+    g.zface_lo, g.zface_hi = box.zface_lo, box.zface_hi
+    tf = torch.from_numpy(dense.view(np.int32)).to(device)
+    cm = torch.empty((box.nz, box.ny, box.nx), dtype=torch.int32, device=device)
+    tm = torch.empty((box.nz, box.ny, box.nx, 2), dtype=torch.int32, device=device)
+    big = np.iinfo(np.int32).max
+    err = torch.tensor([big, big, big, big, 0, 0, 0, big], dtype=torch.int32, device=device)
+    registry = blocks[0].data[flags].registry
+    _lib.call("lbm_build_cellmask", ctypes.byref(g), _lib.ptr(tf), _flag_bits(registry),
+              _lib.ptr(cm), _lib.ptr(tm), _lib.ptr(err),
+              _lib.stream_ptr(torch.cuda.current_stream(device)))
+    e = err.cpu().numpy().tolist()
+
+    def where(v):
+        c = v - 1
+        x = c % box.nx
+        y = (c // box.nx) % box.ny
+        z = c // (box.nx * box.ny)
+        return (box.lo[0] + x, box.lo[1] + y, box.lo[2] + z)
+
+    if e[0] != big:
+        raise ValidationError(f"cell {where(e[0])} carries conflicting boundary flags")
+    if e[1] != big:
+        raise ValidationError(f"fluid cell {where(e[1])} streams from a Solid cell; flag the "
+                              "obstacle surface NoSlip/UBB/Pressure")
+    if e[2] != big:
+        raise ValidationError(f"fluid cell {where(e[2])} streams from an unflagged cell")
+    if e[7] != big:
+        raise ValidationError(f"fluid cell {where(e[7])} streams from a Fluid-flagged ghost cell "
+                              "outside a non-periodic domain face (not supported on the B200 path)")
+    counts = {NO_SLIP: e[5], UBB: e[4], PRESSURE: e[6]}
+    return Masks(cm, tm, counts, None if e[3] == big else where(e[3]))
+
+
+def decode_links(forest, stencil: Stencil, masks: Masks, flags="flags"):
+    """{block_id: {name: [(i, zs, ys, xs)]}} from device masks, in the
+    reference's format (boundary.py:91-96): i is the direction from the
+    fluid cell into the boundary cell, indices are ghost-inclusive."""
+    box = RankBox(forest)
+    cm = masks.cellmask.cpu().numpy().view(np.uint32)
+    tm = masks.typemask.cpu().numpy().view(np.uint32)
+    fluid = (cm & _lib.MASK_FLUID) != 0
+    out = {}
+    for block, (ox, oy, oz) in zip(box.blocks, box.offsets):
+        g = block.data[flags].g
+        n = forest.cells_per_block
+        sl = (slice(oz, oz + n[2]), slice(oy, oy + n[1]), slice(ox, ox + n[0]))
+        c, t0, t1, fl = cm[sl], tm[sl][..., 0], tm[sl][..., 1], fluid[sl]
+        lists = {name: [] for name in _LINK_FLAGS}
+        for i in range(1, stencil.q):
+            j = stencil.opp[i]                     # pulled direction carrying the link
+            hit = fl & (((c >> j) & 1) != 0)
+            is_ubb = ((t0 >> j) & 1) != 0
+            is_pr = ((t1 >> j) & 1) != 0
+            for name, sel in ((NO_SLIP, hit & ~is_ubb & ~is_pr), (UBB, hit & is_ubb),
+                              (PRESSURE, hit & is_pr)):
+                if sel.any():
+                    zs, ys, xs = np.nonzero(sel)
+                    lists[name].append((i, zs + g, ys + g, xs + g))
+        out[block.id] = lists
+    return out
+
+
+def build_index_lists(forest, stencil: Stencil, flags="flags"):
+    """Boundary links per local block (boundary.py:48-97), computed on the
+    device.  Ghost flags must be current (exchange first; freeze does)."""
+    return decode_links(forest, stencil, build_masks(forest, stencil, flags), flags)
+
+
+class BoundaryHandling:
+    """Boundary configuration plus frozen device link masks (boundary.py:100-152).
+
+    freeze() is collective: it refreshes flag ghosts, then builds the masks.
+    Call it again after editing flags."""
+
+    def __init__(self, forest, stencil: Stencil, *, flags="flags", ubb_velocity=(0.0, 0.0, 0.0),
+                 pressure_density=1.0, reference_density=1.0):
+        if stencil.d != forest.d:
+            raise ValidationError(f"{stencil.name} does not match a {forest.d}D forest")
+        self.forest = forest
+        self.stencil = stencil
+        self.flags_key = flags
+        uw = tuple(float(v) for v in ubb_velocity)
+        if len(uw) == 2:
+            uw = (uw[0], uw[1], 0.0)
+        if len(uw) != 3:
+            raise ValidationError(f"wall velocity needs 2 or 3 components, got {ubb_velocity!r}")
+        self.ubb_velocity = uw
+        self.pressure_density = float(pressure_density)
+        self.reference_density = float(reference_density)
+        self.handler = ensure_flags(forest, flags)
+        self._masks = None
+        self._links = None
+        self.generation = 0
+
+    def freeze(self) -> None:
+        exchange_ghosts(self.forest, [GhostPackInfo(self.flags_key)])
+        self._masks = build_masks(self.forest, self.stencil, self.flags_key)
+        self._flag_snapshot = self._dense_flags()
+        self._links = None
+        self.generation += 1
+        for block in self.forest.local_blocks():
+            block.data[self.flags_key].touched = False
+
+    @property
+    def frozen(self) -> bool:
+        return self._masks is not None
+
+    @property
+    def masks(self) -> Masks:
+        if self._masks is None:
+            raise ValidationError("boundary handling not frozen yet")
+        return self._masks
+
+    @property
+    def links(self):
+        if self._links is None:
+            self._links = decode_links(self.forest, self.stencil, self.masks, self.flags_key)
+        return self._links
+
+    def link_count(self, block) -> int:
+        lists = self.links[block.id]
+        return sum(len(zs) for entries in lists.values() for (_, zs, _, _) in entries)
+
+    def known_mask(self, block) -> np.uint32:
+        registry = block.data[self.flags_key].registry
+        out = np.uint32(0)
+        for name in BOUNDARY_FLAGS:
+            out |= registry[name]
+        return out
+
+    def fluid_mask(self, block) -> np.uint32:
+        return block.data[self.flags_key].registry[FLUID]
+
+    def _dense_flags(self):
+        box = RankBox(self.forest)
+        return box.gather([b.data[self.flags_key].field.view_nosync for b in box.blocks], 1,
+                          np.uint32)
+
+    def check_flags(self) -> None:
+        """Sweep-time guard: the masks are a snapshot of the flags taken at
+        freeze().  The reference re-reads the fluid mask every sweep but keeps
+        the frozen links; a mixed state cannot be expressed by one mask, so
+        edits after freeze() must be followed by another freeze()."""
+        blocks = self.forest.local_blocks()
+        if not any(b.data[self.flags_key].touched for b in blocks):
+            return
+        if not np.array_equal(self._dense_flags(), self._flag_snapshot):
+            raise ValidationError("flags were edited after BoundaryHandling.freeze(); call "
+                                  "freeze() again before the next sweep")
+        for b in blocks:
+            b.data[self.flags_key].touched = False
+
+    def apply(self, block, src, dst) -> None:
+        raise ValidationError("boundary links are fused into the stream-collide kernel on the "
+                              "B200 path; call stream_collide(..., handling=...)")

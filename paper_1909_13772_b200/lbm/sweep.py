@@ -1,0 +1,232 @@
+"""Stream-collide time step on HBM-resident PDF fields.
+
+Drop-in for pkg/src/blocksim/lbm/sweep.py: same functions, arguments,
+validation and results.  One `stream_collide` call is one fused sm_100a
+pass (pull -> bounce-back -> collide) per rank box plus, across ranks, the
+zero-copy halo of the crossing directions; the host arrays of the PDF slot
+are a lazily synced mirror (see field.py / device.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from ..device import DeviceLattice
+from ..errors import NumericsError, TopologyError, ValidationError
+from ..field import FieldDataHandler
+from .boundary import BoundaryHandling
+from .collision import kernel_params
+from .stencil import Stencil
+
+
+class _Mirror:
+    """Hook object installed on the src slot's host Fields."""
+
+    def __init__(self, pdf):
+        self.pdf = pdf
+
+    def host_access(self):
+        lat = self.pdf._lattice
+        if lat is not None:
+            lat.sync_host()
+            lat.host_touched()
+
+
+class PdfField:
+    """Population storage: `key` (src) and `key.dst` host slots plus the
+    device lattice (two HBM buffers) behind them.
+
+    dtype="float32" (B200 extension) stores f - w_i in fp32 and computes in
+    fp64 registers; the host mirror stays fp64."""
+
+    def __init__(self, forest, stencil: Stencil, key="pdf", *, layout="zyxf", ghost_layers=1,
+                 dtype="float64"):
+        if stencil.d != forest.d:
+            raise ValidationError(f"{stencil.name} does not match a {forest.d}D forest")
+        if dtype not in ("float64", "float32"):
+            raise ValidationError(f"dtype must be 'float64' or 'float32', got {dtype!r}")
+        self.forest = forest
+        self.stencil = stencil
+        self.key = key
+        self.dst_key = key + ".dst"
+        self.dtype = dtype
+        forest.register_data(key, FieldDataHandler(nf=stencil.q, ghost_layers=ghost_layers,
+                                                   layout=layout))
+        forest.register_data(self.dst_key, FieldDataHandler(nf=stencil.q, ghost_layers=ghost_layers,
+                                                            layout=layout))
+        self._lattice = None
+        self._mirror = _Mirror(self)
+        for block in forest.local_blocks():
+            block.data[key]._mirror = self._mirror
+        self._kp_cache = {}
+
+    def src(self, block):
+        return block.data[self.key]
+
+    def dst(self, block):
+        return block.data[self.dst_key]
+
+    def swap_all(self) -> None:
+        for block in self.forest.local_blocks():
+            self.src(block).swap_data(self.dst(block))
+
+    @property
+    def lattice(self) -> DeviceLattice:
+        if self._lattice is None:
+            self._lattice = DeviceLattice(self, self.dtype)
+        return self._lattice
+
+    @property
+    def g(self):
+        for block in self.forest.local_blocks():
+            return block.data[self.key].g
+        return 1
+
+    def params(self, model, force, handling):
+        """Cached kernel parameters + the collision identity key."""
+        ck = (id(model), id(force), id(handling))
+        hit = self._kp_cache.get(ck)
+        if hit is not None:
+            return hit[1], hit[2]
+        uw = handling.ubb_velocity if handling is not None else (0.0, 0.0, 0.0)
+        rho0 = handling.reference_density if handling is not None else 1.0
+        kp = kernel_params(self.stencil, model, force, ubb_velocity=uw, reference_density=rho0)
+        if handling is not None:
+            for k in range(self.stencil.q):
+                kp.struct.pressure[k] = 2.0 * self.stencil.weights[k] * handling.pressure_density
+        s = kp.struct
+        key = (bytes(memoryview(s))[:-8], b"" if kp.tables is None else kp.tables.tobytes())
+        # keep the objects alive so their ids cannot be reused
+        self._kp_cache[ck] = ((model, force, handling), kp, key)
+        return kp, key
+
+
+def fill_equilibrium(pdf: PdfField, rho=1.0, velocity=(0.0, 0.0, 0.0)) -> None:
+    """Set the field to the equilibrium of (rho, velocity), ghosts included
+    (sweep.py:51-76).  Callables are evaluated on the host over cell-centre
+    coordinates exactly as the reference does; the equilibrium itself is
+    computed on the device straight into the HBM layout."""
+    forest = pdf.forest
+    lat = pdf.lattice
+    box = lat.box
+    rviews, uviews = [], []
+    for block in box.blocks:
+        field = pdf.src(block)
+        g = field.g
+        (cx0, cy0, cz0), (dx, dy, dz) = forest.cell_centers(block.id)
+        xs = cx0 + dx * (np.arange(field.nx + 2 * g) - g)
+        ys = cy0 + dy * (np.arange(field.ny + 2 * g) - g)
+        zs = cz0 + dz * (np.arange(field.nz + 2 * g) - g)
+        z, y, x = np.meshgrid(zs, ys, xs, indexing="ij")
+        r = rho(x, y, z) if callable(rho) else np.full(x.shape, float(rho))
+        r = np.broadcast_to(np.asarray(r, dtype=np.float64), x.shape)
+        if callable(velocity):
+            u = np.stack(np.broadcast_arrays(*velocity(x, y, z)), axis=-1)
+        else:
+            u = np.broadcast_to(np.asarray(velocity, dtype=np.float64), x.shape + (len(velocity),))
+        u = np.asarray(u, dtype=np.float64)
+        if u.shape[-1] == 2:
+            u = np.concatenate([u, np.zeros(u.shape[:-1] + (1,))], axis=-1)
+        if u.shape[-1] != 3:
+            raise ValidationError(f"velocity needs 2 or 3 components, got shape {u.shape}")
+        rviews.append(r[..., None])
+        uviews.append(u)
+    rho_g = box.gather(rviews, 1, np.float64)[0]
+    u_g = np.moveaxis(box.gather(uviews, 3, np.float64), 0, 3)
+    lat.fill_equilibrium(rho_g, u_g)
+
+
+def _require_uniform(forest) -> None:
+    for block in forest.local_blocks():
+        if block.level != 0:
+            raise TopologyError("stream-collide needs a uniform refinement level")
+
+
+def _prepare(pdf: PdfField, model, force, handling):
+    forest = pdf.forest
+    st = pdf.stencil
+    _require_uniform(forest)
+    if handling is not None and handling.stencil is not st:
+        raise ValidationError("boundary handling built for a different stencil")
+    if handling is None:
+        for a in range(forest.d):
+            if not forest.periodic[a]:
+                raise ValidationError("without boundary handling the domain must be fully periodic")
+    elif not handling.frozen:
+        handling.freeze()
+    if pdf.g != 1:
+        raise ValidationError("stream-collide needs exactly one pdf ghost layer")
+    if getattr(model, "omega_field", None) is not None:
+        raise ValidationError("per-cell SRT rates (omega_field) are not supported on the B200 path yet")
+    lat = pdf.lattice
+    if handling is not None:
+        for block in forest.local_blocks():
+            if block.data[handling.flags_key].g != pdf.g:
+                raise ValidationError("flag and pdf ghost layers differ")
+        handling.check_flags()
+        masks = handling.masks
+        if masks.unflagged_cell is not None:
+            raise ValidationError(f"unflagged cell {masks.unflagged_cell}")
+    else:
+        masks = lat.default_masks()
+    kp, key = pdf.params(model, force, handling)
+    key = key + (id(masks),)
+    if lat.host_changed():
+        lat.upload_host()
+    return lat, kp, key, masks
+
+
+def stream_collide(pdf: PdfField, model, *, force=None, handling=None) -> None:
+    """Advance the lattice by one time step (collective, sweep.py:93-151)."""
+    lat, kp, key, masks = _prepare(pdf, model, force, handling)
+    lat.step(kp, key, masks, 1)
+
+
+def stream_collide_n(pdf: PdfField, model, steps, *, force=None, handling=None) -> None:
+    """`steps` calls of stream_collide with one validation pass (B200
+    extension for long time loops; bitwise identical to the loop)."""
+    if steps < 0:
+        raise ValidationError("steps must be >= 0")
+    if steps == 0:
+        return
+    lat, kp, key, masks = _prepare(pdf, model, force, handling)
+    lat.step(kp, key, masks, int(steps))
+
+
+def macroscopic_fields(pdf: PdfField, density="rho", velocity="vel", *, force=None,
+                       handling=None) -> None:
+    """Per-cell density and velocity of fluid cells into registered fields
+    (sweep.py:154-176), computed on the device from the current R-form."""
+    forest = pdf.forest
+    lat = pdf.lattice
+    if lat.host_changed():
+        lat.upload_host()
+    from .collision import SRT, Guo, kernel_params as _kp
+    kp = _kp(pdf.stencil, SRT(1.0), force if isinstance(force, Guo) else None)
+    masks = lat.stream_masks or lat.default_masks()
+    rho_t, u_t, bad = lat.moments(kp, masks)
+    if int(bad.item()):
+        raise NumericsError(f"non-positive density {float(rho_t.min().item())}")
+    rho = rho_t.cpu().numpy()
+    u = u_t.cpu().numpy()
+    box = lat.box
+    for block, (ox, oy, oz) in zip(box.blocks, box.offsets):
+        n = forest.cells_per_block
+        sl = (slice(oz, oz + n[2]), slice(oy, oy + n[1]), slice(ox, ox + n[0]))
+        if handling is not None:
+            flags = block.data[handling.flags_key]
+            fluid = (flags.field.interior[..., 0] & handling.fluid_mask(block)) != 0
+        else:
+            fluid = slice(None)
+        if density is not None:
+            block.data[density].interior[..., 0][fluid] = rho[sl][fluid]
+        if velocity is not None:
+            out = block.data[velocity].interior
+            for a in range(out.shape[-1]):
+                out[..., a][fluid] = u[sl][..., a][fluid]
+
+
+def mlups(interior_cells, steps, seconds) -> float:
+    """Million lattice-cell updates per second (sweep.py:179-183)."""
+    if seconds <= 0.0:
+        raise ValidationError(f"need a positive wall time, got {seconds}")
+    return interior_cells * steps / seconds / 1.0e6

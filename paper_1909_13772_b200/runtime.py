@@ -1,0 +1,141 @@
+"""Rank context: one process per GPU over torch.distributed.
+
+Replaces the reference's simulated runtime (SimRuntime / RankContext,
+pkg/src/blocksim/runtime/core.py:56-121,124-218) for the calls the LBM path
+makes: `rank`, `n_ranks`, `all_gather`, `all_reduce`, `barrier`.  The
+per-step halo traffic does not go through this object's Python API; it is a
+zero-copy NCCL send/recv of field slices (see halo.py).
+"""
+from __future__ import annotations
+
+import os
+import pickle
+import socket
+
+import torch
+import torch.distributed as dist
+
+from .errors import ValidationError
+
+
+class Context:
+    """Per-rank handle.  Single process when torch.distributed is not
+    initialised (n_ranks == 1)."""
+
+    def __init__(self, device=None):
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank()
+            self.n_ranks = dist.get_world_size()
+            self.backend = dist.get_backend()
+        else:
+            self.rank, self.n_ranks, self.backend = 0, 1, None
+        if device is None:
+            if torch.cuda.is_available():
+                local = int(os.environ.get("LOCAL_RANK", self.rank % max(1, torch.cuda.device_count())))
+                device = torch.device("cuda", local)
+            else:
+                device = torch.device("cpu")
+        self.device = torch.device(device)
+        self.step = 0
+
+    @property
+    def distributed(self) -> bool:
+        return self.n_ranks > 1
+
+    def all_gather(self, obj) -> dict:
+        """{rank: obj} from every rank (RankContext.all_gather, core.py:95-100)."""
+        if self.n_ranks == 1:
+            return {0: pickle.loads(pickle.dumps(obj))}
+        out = [None] * self.n_ranks
+        dist.all_gather_object(out, obj)
+        return {r: out[r] for r in range(self.n_ranks)}
+
+    def all_reduce(self, values, op: str = "sum"):
+        """Element-wise reduction folded in ascending rank order (core.py:82-93)."""
+        scalar = isinstance(values, (int, float))
+        vec = [float(values)] if scalar else [float(v) for v in values]
+        gathered = self.all_gather(vec)
+        acc = list(gathered[0])
+        for r in range(1, self.n_ranks):
+            for k, v in enumerate(gathered[r]):
+                if op == "sum":
+                    acc[k] = acc[k] + v
+                elif op == "max":
+                    acc[k] = max(acc[k], v)
+                elif op == "min":
+                    acc[k] = min(acc[k], v)
+                else:
+                    raise ValidationError(f"unknown reduction {op!r}")
+        return acc[0] if scalar else acc
+
+    def barrier(self) -> None:
+        if self.n_ranks > 1:
+            dist.barrier()
+
+    def advance_step(self) -> int:
+        self.step += 1
+        return self.step
+
+
+def init_distributed(backend: str | None = None) -> Context:
+    """Initialise torch.distributed from the torchrun environment (RANK,
+    WORLD_SIZE, MASTER_ADDR, MASTER_PORT) and return the rank context."""
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1 and not dist.is_initialized():
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend=backend)
+    return Context()
+
+
+# ------------------------------------------------- local multi-process runs
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, n_ranks, port, backend, program, args, queue):
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
+                       "RANK": str(rank), "WORLD_SIZE": str(n_ranks), "LOCAL_RANK": str(rank)})
+    try:
+        dist.init_process_group(backend=backend, rank=rank, world_size=n_ranks)
+        ctx = Context(device="cpu" if backend == "gloo" else None)
+        res = program(ctx, *args)
+        queue.put((rank, "ok", res))
+    except BaseException as exc:  # report, do not hang the parent
+        import traceback
+        queue.put((rank, "error", f"{type(exc).__name__}: {exc}\n{traceback.format_exc()}"))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def run(n_ranks: int, program, *args, backend: str = "gloo", timeout: float = 600.0):
+    """Run `program(ctx, *args)` on `n_ranks` local processes (SimRuntime.run's
+    role in the reference tests).  Returns the per-rank results in rank order."""
+    import torch.multiprocessing as mp
+    if n_ranks == 1:
+        return [program(Context(), *args)]
+    ctxmp = mp.get_context("spawn")
+    queue = ctxmp.Queue()
+    port = _free_port()
+    procs = [ctxmp.Process(target=_worker, args=(r, n_ranks, port, backend, program, args, queue))
+             for r in range(n_ranks)]
+    for p in procs:
+        p.start()
+    results, errors = {}, []
+    for _ in range(n_ranks):
+        rank, status, payload = queue.get(timeout=timeout)
+        if status == "ok":
+            results[rank] = payload
+        else:
+            errors.append(payload)
+    for p in procs:
+        p.join(timeout=60)
+    if errors:
+        raise RuntimeError("rank failed:\n" + "\n".join(errors))
+    return [results[r] for r in range(n_ranks)]

@@ -1,0 +1,131 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the container that holds /root/reference (read-only):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports blocksim from /root/reference/pkg/src, drives every case of
+tests/cases.py through the reference's own sweep API under SimRuntime
+(1 rank, plus 2 ranks where the partition allows, asserting the reference's
+bitwise rank invariance), and writes:
+
+  golden/<case>.npz      snapshots of the gathered R-form PDFs (z,y,x,q),
+                         macroscopic fields, link counts, sha256 digests
+  golden/digests.json    sha256 of larger cases (no arrays committed)
+  golden/units.npz       reference unit outputs: collide_pdfs for every model
+                         variant, equilibrium/macroscopic, TRT magic rates,
+                         moment bases, guo_matrix
+
+Nothing here runs on the GPU box (/root/reference does not exist there);
+the committed files are what the tests read.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+os.environ.setdefault("BLOCKSIM_KERNELS", "python")
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import cases  # noqa: E402
+from blocksim.runtime import SimRuntime  # noqa: E402
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def run_ref(spec, n_ranks=1):
+    api = cases.reference_api()
+    return SimRuntime(n_ranks, seed=0).run(lambda ctx: cases.run_case(api, ctx, spec))[0]
+
+
+def main():
+    meta = {}
+    for name, spec in cases.CASES.items():
+        res = run_ref(spec)
+        if spec["root_dims"][2] >= 2 or spec["root_dims"][0] >= 2:
+            res2 = run_ref(spec, 2)
+            for s in res["pdf"]:
+                assert res["pdf"][s].tobytes() == res2["pdf"][s].tobytes(), f"{name}: rank variance"
+        arrays = {}
+        digests = {}
+        for s, arr in res["pdf"].items():
+            arrays[f"pdf_{s}"] = arr
+            digests[f"pdf_{s}"] = sha(arr)
+        if res["macro"] is not None:
+            arrays["rho"], arrays["vel"] = res["macro"]
+            digests["rho"], digests["vel"] = sha(res["macro"][0]), sha(res["macro"][1])
+        links = res["links"] or {}
+        np.savez(HERE / f"{name}.npz", **arrays)
+        meta[name] = {"digests": digests, "links": links, "spec": repr(spec)}
+        print(name, {k: v[:12] for k, v in digests.items()}, links, flush=True)
+    dig = {}
+    for name, spec in cases.DIGEST_CASES.items():
+        res = run_ref(spec)
+        dig[name] = {f"pdf_{s}": sha(a) for s, a in res["pdf"].items()}
+        dig[name]["links"] = res["links"]
+        print(name, dig[name], flush=True)
+    meta["digest_cases"] = dig
+    (HERE / "digests.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
+    make_units()
+
+
+def make_units():
+    """Reference unit functions on seeded random cells."""
+    import blocksim.lbm as L
+    from blocksim.lbm.collision import _kernel_params
+    out = {}
+    rng = np.random.default_rng(2024)
+    for st in (L.D2Q9, L.D3Q19, L.D3Q27):
+        n = 64
+        rho = rng.uniform(0.5, 2.0, n)
+        u = rng.uniform(-0.1, 0.1, (n, 3))
+        if st.d == 2:
+            u[:, 2] = 0.0
+        f = L.equilibrium(rho, u, st)
+        f *= 1.0 + 0.05 * rng.uniform(-1.0, 1.0, f.shape)
+        out[f"{st.name}_in"] = f
+        out[f"{st.name}_eq_rho"], out[f"{st.name}_eq_u"] = rho, u
+        out[f"{st.name}_eq"] = L.equilibrium(rho, u, st)
+        r, v = L.macroscopic(f, st)
+        out[f"{st.name}_macro_rho"], out[f"{st.name}_macro_u"] = r, v
+        r, v = L.macroscopic(f, st, force=L.Guo((3e-4, -2e-4, 1e-4)))
+        out[f"{st.name}_macroguo_rho"], out[f"{st.name}_macroguo_u"] = r, v
+        variants = {"srt": L.SRT(1.3), "trt": L.TRT(1.3, 0.9), "trtmagic": L.TRT.with_magic(1.7)}
+        if st.name != "D3Q27":
+            variants["mrtu"] = L.MRT.uniform(st, 1.3)
+            if st.name == "D3Q19":
+                rates = [1.0] * st.q
+                rates[9:16] = [1.4] * 7
+                variants["mrt"] = L.MRT(st, rates)
+        forces = {"none": None, "guo": L.Guo((3e-4, -2e-4, 1e-4))}
+        for vn, model in variants.items():
+            for fn, force in forces.items():
+                out[f"{st.name}_{vn}_{fn}"] = L.collide_pdfs(f, st, model, force)
+            if isinstance(model, L.MRT):
+                p = _kernel_params(st, model, L.Guo((3e-4, -2e-4, 1e-4)))
+                out[f"{st.name}_{vn}_guo_matrix"] = p["guo_matrix"]
+        out[f"{st.name}_srt_shift"] = L.collide_pdfs(f, st, L.SRT(1.3),
+                                                     L.SimpleShift((3e-4, -2e-4, 1e-4)))
+    for st in (L.D2Q9, L.D3Q19):
+        out[f"{st.name}_M"] = L.moment_basis(st)
+        out[f"{st.name}_Minv"] = L.basis_inverse(L.moment_basis(st))
+    out["magic_omegas"] = np.array([L.TRT.with_magic(w).omega_o for w in (0.6, 1.0, 1.4, 1.7, 1.8)])
+    out["equilibrium_hand"] = L.equilibrium(1.0, (0.1, 0.0), L.D2Q9)
+    np.savez(HERE / "units.npz", **out)
+    print("units:", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()
