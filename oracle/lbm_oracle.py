@@ -347,3 +347,15 @@ def threads_available():
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def collide_cells(st: OStencil, f, model: Model):
+    """impl.collide on a flat (n, q) population array (returns a copy)."""
+    f = np.asarray(f, dtype=np.float64)
+    n = f.shape[0]
+    pdf = np.ascontiguousarray(f.T.reshape(st.q, 1, 1, n)).copy()
+    flags = np.ones((1, 1, n), dtype=np.uint32)
+    cst = _cstencil(st)
+    cp = model.cparams()
+    lib().orc_collide(ctypes.byref(cst), _ptr(pdf), _ptr(flags), 1, n, 1, 1, ctypes.byref(cp))
+    return pdf.reshape(st.q, n).T.copy()

@@ -179,6 +179,7 @@ class DeviceLattice:
         self.host_state = "host"  # "host": host authoritative; "device": host stale; "synced"
         self.snapshot = None
         self.steps = 0
+        self.launches = 0         # fused-kernel launches issued (bench's gpu_launches)
         self._halo = None
         self._streams = None
         self._fluid_masks = None
@@ -202,6 +203,20 @@ class DeviceLattice:
     # ------------------------------------------------------ host <-> HBM
     def upload_host(self):
         """Host R-form (src slot, ghosts incl.) -> buffer[cur] (kind R)."""
+        fields = [b.data[self.pdf.key] for b in self.box.blocks]
+        if not any(f.allocated for f in fields):
+            # never written on the host: the reference's fields start at 0.0
+            b = self.box
+            z = torch.zeros((b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64, device=self.device)
+            zu = torch.zeros((b.nz + 2, b.ny + 2, b.nx + 2, 3), dtype=torch.float64,
+                             device=self.device)
+            _lib.call("lbm_fill_equilibrium", self.gref, _lib.ptr(z), _lib.ptr(zu),
+                      _lib.ptr(self.buf[self.cur]), self._sp())
+            self.cur_kind, self.prev_kind = "R", None
+            self.coll_key = None
+            self.host_state = "device"
+            self.snapshot = None
+            return
         dense = self.box.gather(self._views(self.pdf.key), self.q, np.float64)
         t = torch.from_numpy(dense).pin_memory().to(self.device, non_blocking=True)
         _lib.call("lbm_pack_rform", self.gref, _lib.ptr(t), _lib.ptr(self.buf[self.cur]), self._sp())
@@ -358,6 +373,7 @@ class DeviceLattice:
             self.cur = 1 - self.cur
             self.prev_kind = "G"
             self.steps += 1
+            self.launches += 1 if not self.has_halo else len({0, nz - 1}) + (1 if nz > 2 else 0)
         self.stream_masks = masks
         self._kp_stream = kp
         self.host_state = "device"

@@ -21,9 +21,10 @@ LAYOUTS = ("zyxf", "fzyx")
 class Field:
     """(nx, ny, nz, nf) values plus g ghost layers, layout "zyxf" or "fzyx"."""
 
-    __slots__ = ("nx", "ny", "nz", "nf", "g", "layout", "dx", "_raw", "_mirror")
+    __slots__ = ("nx", "ny", "nz", "nf", "g", "layout", "dx", "_raw_", "_mirror", "_lazy")
 
-    def __init__(self, dims, ghost_layers=0, layout="zyxf", init=0.0, dtype=np.float64, dx=1.0):
+    def __init__(self, dims, ghost_layers=0, layout="zyxf", init=0.0, dtype=np.float64, dx=1.0,
+                 lazy=False):
         nx, ny, nz, nf = (int(v) for v in dims)
         if min(nx, ny, nz, nf) < 1:
             raise ValidationError(f"field dims must be positive, got {dims}")
@@ -37,8 +38,26 @@ class Field:
         self.dx = float(dx)
         g2 = 2 * self.g
         shape = (nz + g2, ny + g2, nx + g2, nf) if layout == "zyxf" else (nf, nz + g2, ny + g2, nx + g2)
-        self._raw = np.full(shape, init, dtype=dtype)
+        # lazy: the host copy of an HBM-resident field is only allocated
+        # when the host actually touches it (a 512^3 D3Q19 field is 21 GB)
+        self._lazy = (shape, init, dtype) if lazy else None
+        self._raw_ = None if lazy else np.full(shape, init, dtype=dtype)
         self._mirror = None
+
+    @property
+    def _raw(self):
+        if self._raw_ is None:
+            shape, init, dtype = self._lazy
+            self._raw_ = np.full(shape, init, dtype=dtype)
+        return self._raw_
+
+    @_raw.setter
+    def _raw(self, value):
+        self._raw_ = value
+
+    @property
+    def allocated(self) -> bool:
+        return self._raw_ is not None
 
     # device mirror hook: sync before handing the array out
     @property
@@ -174,19 +193,21 @@ def sweep(forest, kernel) -> None:
 class FieldDataHandler:
     """Creates one Field per block (handler.py:36-67)."""
 
-    def __init__(self, nf=1, ghost_layers=1, layout="zyxf", init=0.0, dtype=np.float64):
+    def __init__(self, nf=1, ghost_layers=1, layout="zyxf", init=0.0, dtype=np.float64,
+                 lazy=False):
         self.nf = int(nf)
         self.g = int(ghost_layers)
         self.layout = layout
         self.init = init
         self.dtype = dtype
+        self.lazy = lazy
 
     def create(self, forest, block) -> Field:
         if forest.cells_per_block is None:
             raise ValidationError("forest has no cells_per_block")
         dx = forest.dx(block.level)[0]
         return Field(tuple(forest.cells_per_block) + (self.nf,), self.g, self.layout, self.init,
-                     self.dtype, dx)
+                     self.dtype, dx, lazy=self.lazy)
 
 
 class FlagFieldHandler:

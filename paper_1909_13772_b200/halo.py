@@ -60,15 +60,35 @@ def plan_ops(zface_lo, zface_hi, lo_peer, hi_peer, spans):
 
 def run_ops(ops, flat, group=None):
     """Issue the grouped send/recv on views of the flat field tensor and
-    return the works (the caller's current stream waits on them)."""
+    return the works (the caller's current stream waits on them).
+
+    With NCCL the views are sent/received in place.  With gloo (CPU test
+    transport) CUDA views are staged through host copies; this keeps the
+    multi-process tests runnable with several ranks sharing one GPU, where
+    NCCL cannot run."""
     if not ops:
         return []
-    p2p = []
+    staged = flat.is_cuda and dist.get_backend(group) != "nccl"
+    p2p, back = [], []
     for kind, peer, off, count in ops:
         view = flat[off:off + count]
+        if staged:
+            if kind == "send":
+                view = view.cpu()
+            else:
+                host = view.new_empty(view.shape, device="cpu")
+                back.append((flat[off:off + count], host))
+                view = host
         fn = dist.isend if kind == "send" else dist.irecv
         p2p.append(dist.P2POp(fn, view, peer, group))
-    return dist.batch_isend_irecv(p2p)
+    works = dist.batch_isend_irecv(p2p)
+    if staged:
+        for w in works:
+            w.wait()
+        for dst, host in back:
+            dst.copy_(host)
+        return []
+    return works
 
 
 class Halo:

@@ -50,9 +50,9 @@ class PdfField:
         self.dst_key = key + ".dst"
         self.dtype = dtype
         forest.register_data(key, FieldDataHandler(nf=stencil.q, ghost_layers=ghost_layers,
-                                                   layout=layout))
+                                                   layout=layout, lazy=True))
         forest.register_data(self.dst_key, FieldDataHandler(nf=stencil.q, ghost_layers=ghost_layers,
-                                                            layout=layout))
+                                                            layout=layout, lazy=True))
         self._lattice = None
         self._mirror = _Mirror(self)
         for block in forest.local_blocks():
@@ -133,6 +133,56 @@ def fill_equilibrium(pdf: PdfField, rho=1.0, velocity=(0.0, 0.0, 0.0)) -> None:
     rho_g = box.gather(rviews, 1, np.float64)[0]
     u_g = np.moveaxis(box.gather(uviews, 3, np.float64), 0, 3)
     lat.fill_equilibrium(rho_g, u_g)
+
+
+def fill_equilibrium_arrays(pdf: PdfField, rho, u) -> None:
+    """B200 extension: equilibrium of per-cell arrays of this rank's box,
+    rho (nz, ny, nx) and u (nz, ny, nx, 3) (host numpy / pinned or device
+    tensors).  Ghost cells take the nearest interior value.  One H2D copy of
+    32 bytes per cell, the equilibrium is evaluated on the device."""
+    import torch
+    lat = pdf.lattice
+    b = lat.box
+    dev = lat.device
+    tr = torch.empty((b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64, device=dev)
+    tu = torch.empty((b.nz + 2, b.ny + 2, b.nx + 2, 3), dtype=torch.float64, device=dev)
+    r = rho if isinstance(rho, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rho))
+    v = u if isinstance(u, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(u))
+    if tuple(r.shape) != (b.nz, b.ny, b.nx) or tuple(v.shape) != (b.nz, b.ny, b.nx, 3):
+        raise ValidationError("rho / u must cover this rank's box: "
+                              f"({b.nz}, {b.ny}, {b.nx}) and (..., 3)")
+    tr[1:-1, 1:-1, 1:-1].copy_(r, non_blocking=True)
+    tu[1:-1, 1:-1, 1:-1].copy_(v, non_blocking=True)
+    for t in (tr, tu):
+        t[0] = t[1]
+        t[-1] = t[-2]
+        t[:, 0] = t[:, 1]
+        t[:, -1] = t[:, -2]
+        t[:, :, 0] = t[:, :, 1]
+        t[:, :, -1] = t[:, :, -2]
+    from .. import _lib
+    _lib.call("lbm_fill_equilibrium", lat.gref, _lib.ptr(tr), _lib.ptr(tu),
+              _lib.ptr(lat.buf[lat.cur]), lat._sp())
+    lat.cur_kind, lat.prev_kind, lat.coll_key = "R", None, None
+    lat.host_state, lat.snapshot = "device", None
+
+
+def macroscopic_arrays(pdf: PdfField, *, force=None, out=None):
+    """B200 extension: (rho, u) of this rank's box as device tensors, or
+    copied into `out = (rho_host, u_host)` (e.g. pinned) - the D2H half of
+    an end-to-end run.  Raises NumericsError on a non-positive density."""
+    lat = pdf.lattice
+    if lat.host_changed():
+        lat.upload_host()
+    from .collision import SRT, Guo, kernel_params as _kp
+    kp = _kp(pdf.stencil, SRT(1.0), force if isinstance(force, Guo) else None)
+    rho_t, u_t, bad = lat.moments(kp, lat.stream_masks or lat.default_masks())
+    if out is not None:
+        out[0].copy_(rho_t)
+        out[1].copy_(u_t)
+    if int(bad.item()):
+        raise NumericsError(f"non-positive density {float(rho_t.min().item())}")
+    return (rho_t, u_t) if out is None else out
 
 
 def _require_uniform(forest) -> None:

@@ -98,12 +98,17 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, n_ranks, port, backend, program, args, queue):
+def _worker(rank, n_ranks, port, backend, device, program, args, queue):
     os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
                        "RANK": str(rank), "WORLD_SIZE": str(n_ranks), "LOCAL_RANK": str(rank)})
     try:
         dist.init_process_group(backend=backend, rank=rank, world_size=n_ranks)
-        ctx = Context(device="cpu" if backend == "gloo" else None)
+        if device is None:
+            device = "cpu" if backend == "gloo" else None
+        if device == "cuda":
+            device = torch.device("cuda", rank % torch.cuda.device_count())
+            torch.cuda.set_device(device)
+        ctx = Context(device=device)
         res = program(ctx, *args)
         queue.put((rank, "ok", res))
     except BaseException as exc:  # report, do not hang the parent
@@ -114,16 +119,20 @@ def _worker(rank, n_ranks, port, backend, program, args, queue):
             dist.destroy_process_group()
 
 
-def run(n_ranks: int, program, *args, backend: str = "gloo", timeout: float = 600.0):
+def run(n_ranks: int, program, *args, backend: str = "gloo", device=None,
+        timeout: float = 600.0):
     """Run `program(ctx, *args)` on `n_ranks` local processes (SimRuntime.run's
-    role in the reference tests).  Returns the per-rank results in rank order."""
+    role in the reference tests).  Returns the per-rank results in rank order.
+    backend="gloo", device="cuda" runs several ranks on the GPUs present
+    (ranks may share one GPU; halos are then staged through the host)."""
     import torch.multiprocessing as mp
     if n_ranks == 1:
-        return [program(Context(), *args)]
+        return [program(Context(device=device if device != "cuda" else None), *args)]
     ctxmp = mp.get_context("spawn")
     queue = ctxmp.Queue()
     port = _free_port()
-    procs = [ctxmp.Process(target=_worker, args=(r, n_ranks, port, backend, program, args, queue))
+    procs = [ctxmp.Process(target=_worker,
+                           args=(r, n_ranks, port, backend, device, program, args, queue))
              for r in range(n_ranks)]
     for p in procs:
         p.start()

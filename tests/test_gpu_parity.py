@@ -1,0 +1,330 @@
+"""GPU parity: the sm_100a path against the reference's golden vectors and the
+pinned CPU oracle, through the public drop-in API (which calls the C-ABI).
+
+fp64 results must be bit-identical (the fp64 kernels round every operation
+like the reference's numpy ufuncs); the BASELINE tolerance (max-abs 1e-12)
+is therefore never needed but is what a failure message reports against.
+fp32 storage is checked at 1e-5 relative against the fp64 oracle.
+"""
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import cases
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+META = json.loads((GOLDEN / "digests.json").read_text())
+UNITS = np.load(GOLDEN / "units.npz")
+TOL_F64 = 1e-12      # BASELINE.json: max-abs on PDFs/rho/u in fp64
+TOL_F32_REL = 1e-5   # BASELINE.json: relative in fp32
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def api():
+    import paper_1909_13772_b200 as P
+    P._lib.load()
+    return cases.b200_api()
+
+
+def _ctx():
+    import paper_1909_13772_b200 as P
+    return P.Context()
+
+
+@pytest.mark.parametrize("name", sorted(cases.CASES))
+def test_cases_bitwise_vs_reference_golden(api, name):
+    spec = cases.CASES[name]
+    res = cases.run_case(api, _ctx(), spec)
+    gold = np.load(GOLDEN / f"{name}.npz")
+    for s, arr in res["pdf"].items():
+        ref = gold[f"pdf_{s}"]
+        d = float(np.abs(arr - ref).max())
+        assert arr.tobytes() == ref.tobytes(), f"{name} step {s}: max|d| = {d:.3e} (tol {TOL_F64})"
+    if res["macro"] is not None:
+        assert res["macro"][0].tobytes() == gold["rho"].tobytes()
+        assert res["macro"][1].tobytes() == gold["vel"].tobytes()
+    if META[name]["links"]:
+        assert res["links"] == META[name]["links"]
+
+
+@pytest.mark.parametrize("name", sorted(cases.DIGEST_CASES))
+def test_digest_cases(api, name):
+    spec = cases.DIGEST_CASES[name]
+    res = cases.run_case(api, _ctx(), spec)
+    for s, arr in res["pdf"].items():
+        assert sha(arr) == META["digest_cases"][name][f"pdf_{s}"]
+
+
+@pytest.mark.parametrize("sname", ["D2Q9", "D3Q19", "D3Q27"])
+def test_flat_cell_kernels_bitwise(api, sname):
+    st = getattr(api, sname)
+    f = UNITS[f"{sname}_in"]
+    variants = {"srt": api.SRT(1.3), "trt": api.TRT(1.3, 0.9), "trtmagic": api.TRT.with_magic(1.7)}
+    if sname != "D3Q27":
+        variants["mrtu"] = api.MRT.uniform(st, 1.3)
+        if sname == "D3Q19":
+            r = [1.0] * 19
+            r[9:16] = [1.4] * 7
+            variants["mrt"] = api.MRT(st, r)
+    for vn, m in variants.items():
+        assert api.collide_pdfs(f, st, m).tobytes() == UNITS[f"{sname}_{vn}_none"].tobytes(), vn
+        got = api.collide_pdfs(f, st, m, api.Guo((3e-4, -2e-4, 1e-4)))
+        assert got.tobytes() == UNITS[f"{sname}_{vn}_guo"].tobytes(), vn
+    got = api.collide_pdfs(f, st, api.SRT(1.3), api.SimpleShift((3e-4, -2e-4, 1e-4)))
+    assert got.tobytes() == UNITS[f"{sname}_srt_shift"].tobytes()
+    eq = api.equilibrium(UNITS[f"{sname}_eq_rho"], UNITS[f"{sname}_eq_u"], st)
+    assert eq.tobytes() == UNITS[f"{sname}_eq"].tobytes()
+    r, u = api.macroscopic(f, st)
+    assert r.tobytes() == UNITS[f"{sname}_macro_rho"].tobytes()
+    assert u.tobytes() == UNITS[f"{sname}_macro_u"].tobytes()
+    r, u = api.macroscopic(f, st, force=api.Guo((3e-4, -2e-4, 1e-4)))
+    assert u.tobytes() == UNITS[f"{sname}_macroguo_u"].tobytes()
+
+
+def test_reference_unit_properties(api):
+    """SRT omega=1 lands exactly on feq; zero force == unforced bitwise
+    (pkg/tests/test_lbm.py:180-184, 239-248); non-positive density raises."""
+    st = api.D2Q9
+    f = UNITS["D2Q9_in"]
+    rho, u = api.macroscopic(f, st)
+    assert np.array_equal(api.collide_pdfs(f, st, api.SRT(1.0)), api.equilibrium(rho, u, st))
+    for m in (api.SRT(1.3), api.TRT(1.3, 0.9), api.MRT.uniform(st, 1.3)):
+        assert np.array_equal(api.collide_pdfs(f, st, m),
+                              api.collide_pdfs(f, st, m, api.Guo((0.0, 0.0, 0.0))))
+    import paper_1909_13772_b200 as P
+    with pytest.raises(P.NumericsError):
+        api.macroscopic(np.zeros(9), st)
+
+
+def _oracle_compare(api, spec, every=None):
+    """Run spec on the GPU and the oracle, compare every snapshot bitwise."""
+    res = cases.run_case(api, _ctx(), spec)
+    ores = cases.oracle_run(spec, oracle)
+    for s in spec["snapshots"]:
+        a, b = res["pdf"][s], ores["pdf"][s]
+        d = float(np.abs(a - b).max())
+        assert a.tobytes() == b.tobytes(), f"step {s}: max|d| = {d:.3e} (tol {TOL_F64})"
+    return res, ores
+
+
+def test_config0_full_size_bitwise(api):
+    """BASELINE config 0: D3Q19 SRT 1.8, 64^3 periodic, seeded random
+    init, 100 steps, compare PDFs every 10 steps."""
+    spec = dict(stencil="D3Q19", dims=(64, 64, 64), root_dims=(1, 1, 1),
+                periodic=(True, True, True), geometry=None, model=("SRT", 1.8), force=None,
+                init=("random", 0), steps=100, snapshots=tuple(range(10, 101, 10)), layout="fzyx")
+    _oracle_compare(api, spec)
+
+
+def test_config1_full_size_bitwise(api):
+    """BASELINE config 1 at full size (128^3 porous, 25 % spheres r 4-8, NoSlip
+    z walls, TRT magic 1.7, Guo 1e-6); 100 of its 1000 steps (oracle cost),
+    plus rho/u."""
+    spec = dict(stencil="D3Q19", dims=(128, 128, 128), root_dims=(1, 1, 1),
+                periodic=(True, True, False),
+                geometry=dict(kind="spheres", seed=1, rmin=4.0, rmax=8.0, frac=0.25, walls_z=True),
+                model=("TRT_magic", 1.7), force=("Guo", (1e-6, 0.0, 0.0)), init=("rest",),
+                steps=100, snapshots=(50, 100), layout="fzyx")
+    _oracle_compare(api, spec)
+
+
+def test_config2_model_fp64_bitwise(api):
+    """BASELINE config 2 physics (D3Q27 raw-moment MRT shear 1.9 / others 1.0,
+    NoSlip x5 + UBB lid (0.05, 0, 0)) in fp64 at 48^3 against the oracle."""
+    spec = dict(stencil="D3Q27", dims=(48, 48, 48), root_dims=(1, 1, 1),
+                periodic=(False, False, False), geometry=dict(kind="cavity"),
+                model=("MRT_raw", 1.9, 1.0), force=None, init=("rest",),
+                ubb_velocity=(0.05, 0.0, 0.0), steps=60, snapshots=(60,), layout="fzyx")
+    _oracle_compare(api, spec)
+
+
+@pytest.mark.parametrize("spec_name", ["c0", "c1", "c2"])
+def test_fp32_storage_within_1e5_relative(api, spec_name):
+    """fp32 PDFs (stored as f - w_i, fp64 arithmetic) vs the fp64 oracle."""
+    specs = {
+        "c0": dict(stencil="D3Q19", dims=(48, 48, 48), root_dims=(1, 1, 1),
+                   periodic=(True, True, True), geometry=None, model=("TRT_magic", 1.8),
+                   force=None, init=("random", 0), steps=200, snapshots=(200,), layout="fzyx"),
+        "c1": dict(stencil="D3Q19", dims=(64, 64, 64), root_dims=(1, 1, 1),
+                   periodic=(True, True, False),
+                   geometry=dict(kind="spheres", seed=100, rmin=4.0, rmax=8.0, frac=0.2,
+                                 walls_z=True),
+                   model=("TRT_magic", 1.7), force=("Guo", (1e-6, 0.0, 0.0)), init=("random", 2),
+                   steps=200, snapshots=(200,), layout="fzyx"),
+        "c2": dict(stencil="D3Q27", dims=(40, 40, 40), root_dims=(1, 1, 1),
+                   periodic=(False, False, False), geometry=dict(kind="cavity"),
+                   model=("MRT_raw", 1.9, 1.0), force=None, init=("rest",),
+                   ubb_velocity=(0.05, 0.0, 0.0), steps=300, snapshots=(300,), layout="fzyx"),
+    }
+    spec = specs[spec_name]
+    res = cases.run_case(api, _ctx(), spec, pdf_kwargs={"dtype": "float32"})
+    ores = cases.oracle_run(spec, oracle)
+    s = spec["steps"]
+    a, b = res["pdf"][s], ores["pdf"][s]
+    rel = float(np.max(np.abs(a - b) / np.abs(b)))
+    assert rel < TOL_F32_REL, rel
+
+
+@pytest.mark.parametrize("name", ["c1_trt_guo_porous", "c2_d3q27_trt_cavity", "d2q9_pressure_box",
+                                  "d3q19_shift_ghostwalls"])
+def test_link_sets_equal_exhaustive_scan(api, name):
+    """GPU link masks decoded to the reference's lists == exhaustive scan
+    (pkg/tests/test_lbm.py:280-331 scan_links oracle)."""
+    import paper_1909_13772_b200 as P
+    spec = cases.CASES[name]
+    pdf, flags, bits = cases.oracle_inputs(spec, oracle)
+    st = oracle.STENCILS[spec["stencil"]]
+    dom = oracle.Domain(st, spec["dims"], spec["periodic"], cases.oracle_model(spec, oracle),
+                        flags, bits)
+    want = oracle.link_sets(dom.flags, st, bits)
+    ctx = _ctx()
+    nx, ny, nz = spec["dims"]
+    d = 2 if spec["stencil"] == "D2Q9" else 3
+    forest = P.create_forest(ctx, (0, 0, 0, 1, 1, 1), (1, 1, 1), d=d,
+                             periodic=spec["periodic"], cells_per_block=(nx, ny, nz))
+    h = P.ensure_flags(forest)
+    blk = forest.local_blocks()[0]
+    ff = blk.data["flags"]
+    assert [int(h.registry[n]) for n in ("Fluid", "NoSlip", "UBB", "Pressure", "Solid")] == \
+        [1, 2, 4, 8, 16]
+    ff.view[...] = flags
+    handling = P.BoundaryHandling(forest, getattr(P, spec["stencil"]))
+    handling.freeze()
+    lists = handling.links[blk.id]
+    for tname in ("NoSlip", "UBB", "Pressure"):
+        got = []
+        for i, zs, ys, xs in lists[tname]:
+            got.append(np.stack([xs - 1, ys - 1, zs - 1, np.full_like(xs, i)], axis=1))
+        got = np.concatenate(got) if got else np.zeros((0, 4), np.int64)
+        got = got[np.lexsort((got[:, 3], got[:, 0], got[:, 1], got[:, 2]))].astype(np.int32)
+        assert np.array_equal(got, want[tname]), tname
+
+
+def test_validation_errors_mirror_reference(api):
+    import paper_1909_13772_b200 as P
+    ctx = _ctx()
+    forest = P.create_forest(ctx, (0, 0, 0, 1, 1, 1), (1, 1, 1), d=2, periodic=(True, True, False),
+                             cells_per_block=(6, 6, 1))
+    h = P.ensure_flags(forest)
+    ff = forest.local_blocks()[0].data["flags"]
+    ff.interior[...] = h.registry["Fluid"]
+    ff.interior[0, 2, 2] = h.registry["Solid"]
+    handling = P.BoundaryHandling(forest, P.D2Q9)
+    with pytest.raises(P.ValidationError):
+        handling.freeze()                      # fluid streams from Solid
+    ff.interior[0, 2, 2] = 0
+    with pytest.raises(P.ValidationError):
+        handling.freeze()                      # fluid streams from unflagged
+    ff.interior[0, 1:4, 1:4] = h.registry["NoSlip"]
+    ff.interior[0, 2, 2] = h.registry["Solid"]
+    handling.freeze()                          # wrapped in a boundary layer: fine
+    ff.interior[0, 0, 0] |= h.registry["NoSlip"]
+    with pytest.raises(P.ValidationError):
+        handling.freeze()                      # conflicting flags
+    # non-periodic domain without handling
+    f2 = P.create_forest(ctx, (0, 0, 0, 1, 1, 1), (1, 1, 1), d=2, periodic=(True, False, False),
+                         cells_per_block=(4, 4, 1))
+    pdf = P.PdfField(f2, P.D2Q9)
+    P.fill_equilibrium(pdf)
+    with pytest.raises(P.ValidationError):
+        P.stream_collide(pdf, P.SRT(1.2))
+
+
+def test_model_switch_between_sweeps_matches_oracle(api):
+    """Changing the model between calls re-collides the stored state: the
+    result equals the reference's per-call semantics (oracle, bitwise)."""
+    import paper_1909_13772_b200 as P
+    spec = dict(cases.CASES["c0_srt_periodic"])
+    ctx = _ctx()
+    nx, ny, nz = spec["dims"]
+    forest = P.create_forest(ctx, (0, 0, 0, 1, 1, 1), (1, 1, 1), periodic=(True, True, True),
+                             cells_per_block=(nx, ny, nz))
+    pdf = P.PdfField(forest, P.D3Q19, layout="fzyx")
+    P.fill_equilibrium(pdf)
+    rho, u = cases.workloads.random_rho_u((nx, ny, nz), 0)
+    blk = forest.local_blocks()[0]
+    pdf.src(blk).interior[...] = P.equilibrium(rho, u, P.D3Q19)
+    for _ in range(3):
+        P.stream_collide(pdf, P.SRT(1.8))
+    for _ in range(3):
+        P.stream_collide(pdf, P.TRT(1.3, 0.9), force=P.Guo((1e-4, 0, 0)))
+    got = pdf.src(blk).interior.copy()
+    st = oracle.STENCILS["D3Q19"]
+    full, _, _ = cases.oracle_inputs(spec, oracle)
+    d1 = oracle.Domain(st, (nx, ny, nz), (True, True, True), oracle.Model("SRT", omega=1.8))
+    d1.set_full(full)
+    d1.run(3)
+    d2 = oracle.Domain(st, (nx, ny, nz), (True, True, True),
+                       oracle.Model("TRT", omega_e=1.3, omega_o=0.9, force=(1e-4, 0.0, 0.0)))
+    d2.set_full(d1.a)
+    d2.run(3)
+    assert got.tobytes() == d2.rform().tobytes()
+
+
+def test_host_edit_between_sweeps_is_uploaded(api):
+    """A host write into pdf.src(block) after a readout is seen by the next
+    sweep (single-cell bump, pkg/tests/test_lbm.py:436-449 pattern)."""
+    import paper_1909_13772_b200 as P
+    ctx = _ctx()
+    forest = P.create_forest(ctx, (0, 0, 0, 2, 1, 1), (2, 1, 1), d=2, periodic=(True, True, False),
+                             cells_per_block=(8, 8, 1))
+    pdf = P.PdfField(forest, P.D2Q9)
+    P.fill_equilibrium(pdf, 1.0, (0.0, 0.0))
+    P.stream_collide(pdf, P.SRT(1.0))
+    blk = forest.local_blocks()[0]
+    m0 = sum(float(pdf.src(b).interior.sum()) for b in forest.local_blocks())
+    pdf.src(blk).interior[0, 3, 2] = P.equilibrium(1.3, (0.0, 0.0), P.D2Q9)
+    m1 = sum(float(pdf.src(b).interior.sum()) for b in forest.local_blocks())
+    assert m1 > m0 + 0.29
+    for _ in range(5):
+        P.stream_collide(pdf, P.SRT(1.0))
+    m2 = sum(float(pdf.src(b).interior.sum()) for b in forest.local_blocks())
+    assert abs(m2 - m1) < 1e-13
+
+
+# ------------------------------------------------------------ multi-rank
+def _rank_prog(ctx, spec):
+    api = cases.b200_api()
+    return cases.run_case(api, ctx, spec)
+
+
+@pytest.mark.parametrize("n_ranks", [2, 4])
+def test_rank_invariance_bitwise_zslabs(api, n_ranks):
+    """z-slab partition over P ranks (overlapped boundary/interior kernels +
+    halo of crossing directions) == 1 rank, bitwise (test_lbm.py:452-471).
+    Ranks share the one GPU of the test box; the halo is staged over gloo."""
+    import paper_1909_13772_b200 as P
+    spec = dict(stencil="D3Q19", dims=(16, 12, 16), root_dims=(1, 1, 4),
+                periodic=(True, True, False),
+                geometry=dict(kind="spheres", seed=4, rmin=2.0, rmax=3.5, frac=0.2, walls_z=True),
+                model=("TRT_magic", 1.7), force=("Guo", (1e-4, 0.0, 2e-5)), init=("random", 9),
+                steps=12, snapshots=(1, 12), macro=True, layout="fzyx")
+    base = cases.run_case(api, _ctx(), spec)
+    multi = P.run(n_ranks, _rank_prog, spec, backend="gloo", device="cuda")[0]
+    for s in spec["snapshots"]:
+        assert multi["pdf"][s].tobytes() == base["pdf"][s].tobytes(), s
+    assert multi["macro"][0].tobytes() == base["macro"][0].tobytes()
+    assert multi["links"] == base["links"]
+    ores = cases.oracle_run(spec, oracle)
+    assert base["pdf"][12].tobytes() == ores["pdf"][12].tobytes()
+
+
+def test_rank_invariance_periodic_z_two_ranks(api):
+    import paper_1909_13772_b200 as P
+    spec = dict(stencil="D3Q27", dims=(10, 8, 12), root_dims=(1, 1, 2),
+                periodic=(True, True, True), geometry=None, model=("SRT", 1.6), force=None,
+                init=("random", 1), steps=8, snapshots=(8,), layout="zyxf")
+    base = cases.run_case(api, _ctx(), spec)
+    multi = P.run(2, _rank_prog, spec, backend="gloo", device="cuda")[0]
+    assert multi["pdf"][8].tobytes() == base["pdf"][8].tobytes()
+    assert base["pdf"][8].tobytes() == cases.oracle_run(spec, oracle)["pdf"][8].tobytes()
