@@ -121,6 +121,9 @@ typedef struct lbm_params {
 
 /* ------------------------------------------------------------- metadata */
 int lbm_abi_version(void);
+/* sizeof(lbm_grid_t) (which = 0) / sizeof(lbm_params_t) (which = 1), so a
+ * binding can verify its struct mirror; 0 for other values */
+size_t lbm_struct_size(int which);
 const char* lbm_last_error(void);
 /* storage slot of reference direction i (layout above); -1 on bad input */
 int lbm_slot_of(int q, int i);

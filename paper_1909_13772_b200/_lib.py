@@ -21,7 +21,7 @@ MASK_UBB = 0x80000000
 
 # every symbol include/lbm_b200.h declares (tests check the export table)
 EXPORTS = (
-    "lbm_abi_version", "lbm_last_error", "lbm_slot_of", "lbm_field_elems", "lbm_face_span",
+    "lbm_abi_version", "lbm_struct_size", "lbm_last_error", "lbm_slot_of", "lbm_field_elems", "lbm_face_span",
     "lbm_fused_step", "lbm_collide_only", "lbm_stream_only", "lbm_moments",
     "lbm_pack_rform", "lbm_unpack_rform", "lbm_fill_equilibrium", "lbm_build_cellmask",
     "lbm_collide_cells", "lbm_equilibrium_cells", "lbm_macroscopic_cells",
@@ -45,7 +45,7 @@ class Params(ctypes.Structure):
                 ("fx", ctypes.c_double), ("fy", ctypes.c_double), ("fz", ctypes.c_double),
                 ("shift_fx", ctypes.c_double), ("shift_fy", ctypes.c_double),
                 ("shift_fz", ctypes.c_double), ("ubb", ctypes.c_double * 27),
-                ("mrt", ctypes.c_void_p)]
+                ("pressure", ctypes.c_double * 27), ("mrt", ctypes.c_void_p)]
 
 
 _lib = None
@@ -66,6 +66,7 @@ def load(path: Path | None = None):
     G, PR = ctypes.POINTER(Grid), ctypes.POINTER(Params)
     sig = {
         "lbm_abi_version": ([], I),
+        "lbm_struct_size": ([I], ctypes.c_size_t),
         "lbm_last_error": ([], ctypes.c_char_p),
         "lbm_slot_of": ([I, I], I),
         "lbm_field_elems": ([G], I64),
@@ -88,6 +89,10 @@ def load(path: Path | None = None):
         fn.restype = res
     if lib.lbm_abi_version() != 1:
         raise BackendError("kernel library ABI mismatch")
+    if (lib.lbm_struct_size(0) != ctypes.sizeof(Grid)
+            or lib.lbm_struct_size(1) != ctypes.sizeof(Params)):
+        raise BackendError("lbm_grid_t / lbm_params_t layout differs between include/lbm_b200.h "
+                           "and the ctypes mirror")
     _lib = lib
     return lib
 

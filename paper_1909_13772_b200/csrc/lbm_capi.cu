@@ -263,6 +263,10 @@ extern "C" {
 
 int lbm_abi_version(void) { return LBM_B200_ABI_VERSION; }
 
+size_t lbm_struct_size(int which) {
+    return which == 0 ? sizeof(lbm_grid_t) : which == 1 ? sizeof(lbm_params_t) : 0;
+}
+
 const char* lbm_last_error(void) { return g_err; }
 
 int lbm_slot_of(int q, int i) {

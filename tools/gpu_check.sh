@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench=$?
+tail -5 gpurun_out/pytest_gpu.log; tail -3 gpurun_out/bench.log
