@@ -39,6 +39,8 @@ struct Store;
 template <>
 struct Store<double> {
     template <int Q, int I>
+    __device__ __forceinline__ static double widen(double v) { return v; }
+    template <int Q, int I>
     __device__ __forceinline__ static double load(const double* p) { return __ldg(p); }
     template <int Q, int I>
     __device__ __forceinline__ static void store(double* p, double v) { *p = v; }
@@ -46,6 +48,8 @@ struct Store<double> {
 // fp32: stored zero-centred (f - w_i), arithmetic in fp64 registers
 template <>
 struct Store<float> {
+    template <int Q, int I>
+    __device__ __forceinline__ static double widen(float v) { return (double)v + wt<Q, I>(); }
     template <int Q, int I>
     __device__ __forceinline__ static double load(const float* p) {
         return (double)__ldg(p) + wt<Q, I>();
@@ -86,7 +90,7 @@ __device__ __forceinline__ int64_t lidx(const KGrid& g, int z, int slot, int y, 
 // (sequential sums, u = m / rho), then
 //   R[x, i] = -G[x, k] + (2 w_k rho_w) ((1 + (4.5 cu) cu) - 1.5 usq),  k = opp(i).
 template <int Q, typename Real>
-__device__ __noinline__ void pressure_links(const KGrid& g, const KParams& p,
+__device__ __forceinline__ void pressure_links(const KGrid& g, const KParams& p,
                                             const Real* __restrict__ src, int64_t own,
                                             uint32_t pm, double (&f)[Q]) {
     using D = Dirs<Q>;
@@ -123,35 +127,28 @@ __device__ __noinline__ void pressure_links(const KGrid& g, const KParams& p,
 // Load the 19/27/9 pulled populations of cell (x,y,z) with the fused
 // bounce-back substitution R[x,i] = G[x,opp(i)] (- UBB term) for masked
 // directions (boundary.py:163-170).
-template <int Q, typename Real>
-__device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
-                                          const Real* __restrict__ src, int x, int y, int z,
-                                          uint32_t code, const uint32_t* __restrict__ typemask,
-                                          bool generic, double (&f)[Q]) {
+// Element offsets of the pulled sources.  GENERIC (warp-uniform: only warps
+// touching a wrapping edge) applies the covered / uncovered ghost rules;
+// otherwise the source is own - cz*zstride - cy*pitch - cx (+ slot plane).
+template <int Q, bool GENERIC>
+__device__ __forceinline__ void pull_offsets(const KGrid& g, int x, int y, int z, int64_t own,
+                                             int64_t (&off)[Q]) {
     using D = Dirs<Q>;
-    const int64_t own = lidx(g, z, 0, y, x);
-    uint32_t tm = 0, pm = 0;
-    if (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) {
-        const uint2 t = *reinterpret_cast<const uint2*>(typemask + 2 * (((int64_t)z * g.ny + y) * g.nx + x));
-        tm = t.x;
-        pm = t.y;
-    }
-    AxisSrc ax, ay, az;
-    if (generic) {
-        ax = make_axis(x, g.nx, g.wrap_x, !g.wrap_x, !g.wrap_x);
-        ay = make_axis(y, g.ny, g.wrap_y, !g.wrap_y, !g.wrap_y);
-        az = make_axis(z, g.nz, false, g.zlo == LBM_ZFACE_GHOST, g.zhi == LBM_ZFACE_GHOST);
+    if constexpr (!GENERIC) {
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            constexpr int so = slot_of<Q>(i), cx = D::cx[i], cy = D::cy[i], cz = D::cz[i];
+            off[i] = own + (int64_t)so * g.plane - (int64_t)cz * g.zstride - (int64_t)cy * g.pitch - cx;
+        });
+    } else {
+        const AxisSrc ax = make_axis(x, g.nx, g.wrap_x, !g.wrap_x, !g.wrap_x);
+        const AxisSrc ay = make_axis(y, g.ny, g.wrap_y, !g.wrap_y, !g.wrap_y);
+        AxisSrc az = make_axis(z, g.nz, false, g.zlo == LBM_ZFACE_GHOST, g.zhi == LBM_ZFACE_GHOST);
         if (g.zlo == LBM_ZFACE_WRAP && z == 0) az.lo_w = g.nz - 1;
         if (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1) az.hi_w = 0;
-    }
-    static_for<0, Q>([&](auto I_) {
-        constexpr int i = decltype(I_)::value;
-        constexpr int cx = D::cx[i], cy = D::cy[i], cz = D::cz[i];
-        constexpr int so = slot_of<Q>(i);
-        int64_t off;
-        if (!generic) {
-            off = own + (int64_t)so * g.plane - (int64_t)cz * g.zstride - (int64_t)cy * g.pitch - cx;
-        } else {
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            constexpr int cx = D::cx[i], cy = D::cy[i], cz = D::cz[i];
             bool unc = false;
             int xs = x, ys = y, zs = z, xr = x, yr = y, zr = z;
             if constexpr (cx == 1) { xs = ax.lo_w; xr = ax.lo_raw; unc |= ax.lo_unc; }
@@ -160,23 +157,56 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
             if constexpr (cy == -1) { ys = ay.hi_w; yr = ay.hi_raw; unc |= ay.hi_unc; }
             if constexpr (cz == 1) { zs = az.lo_w; zr = az.lo_raw; unc |= az.lo_unc; }
             if constexpr (cz == -1) { zs = az.hi_w; zr = az.hi_raw; unc |= az.hi_unc; }
-            if (unc) { xs = xr; ys = yr; zs = zr; }
-            off = lidx(g, zs, so, ys, xs);
-        }
-        if constexpr (i != 0) {
-            // link: read the own cell's direction k = opp(i) instead (w_k == w_i,
-            // so the fp32 zero-centring offset is the same)
-            constexpr int k = D::opp[i];
-            const bool link = (code >> i) & 1u;
-            if (link) off = own + (int64_t)slot_of<Q>(k) * g.plane;
-            double v = Store<Real>::template load<Q, i>(src + off);
-            if ((tm >> i) & 1u) v = v - p.ubb[k];
-            f[i] = v;
-        } else {
-            f[0] = Store<Real>::template load<Q, 0>(src + off);
-        }
+            xs = unc ? xr : xs;
+            ys = unc ? yr : ys;
+            zs = unc ? zr : zs;
+            off[i] = lidx(g, zs, slot_of<Q>(i), ys, xs);
+        });
+    }
+}
+
+// Three phases so every load of a cell is in flight at once: (1) source
+// offsets with the link substitution folded in as a select, (2) all loads,
+// (3) conversion + the rare UBB / Pressure corrections under one branch.
+template <int Q, typename Real>
+__device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
+                                          const Real* __restrict__ src, int x, int y, int z,
+                                          uint32_t code, const uint32_t* __restrict__ typemask,
+                                          bool generic, double (&f)[Q]) {
+    using D = Dirs<Q>;
+    const int64_t own = lidx(g, z, 0, y, x);
+    int64_t off[Q];
+    if (generic) pull_offsets<Q, true>(g, x, y, z, own, off);
+    else pull_offsets<Q, false>(g, x, y, z, own, off);
+    // link: read the own cell's direction k = opp(i) instead (w_k == w_i, so
+    // the fp32 zero-centring offset is the same)
+    static_for<1, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        constexpr int ks = slot_of<Q>(D::opp[i]);
+        off[i] = ((code >> i) & 1u) ? own + (int64_t)ks * g.plane : off[i];
     });
-    if (pm) pressure_links<Q, Real>(g, p, src, own, pm, f);
+    const bool typed = (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) != 0u;
+    uint2 t = make_uint2(0u, 0u);
+    if (typed) t = __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
+    Real raw[Q];
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        raw[i] = __ldg(src + off[i]);
+    });
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        f[i] = Store<Real>::template widen<Q, i>(raw[i]);
+    });
+    if (typed) {
+        if (t.x) {
+            static_for<1, Q>([&](auto I_) {
+                constexpr int i = decltype(I_)::value;
+                constexpr int k = D::opp[i];
+                if ((t.x >> i) & 1u) f[i] = f[i] - p.ubb[k];
+            });
+        }
+        if (t.y) pressure_links<Q, Real>(g, p, src, own, t.y, f);
+    }
 }
 
 // Fused pull -> bounce-back -> collide over interior planes [z0, z0+gridDim.z).
@@ -205,6 +235,51 @@ __global__ void __launch_bounds__(128) k_fused(KGrid g, KParams p, const Real* _
         constexpr int i = decltype(I_)::value;
         Store<Real>::template store<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
     });
+}
+
+// z-marching variant: one thread per (x, y) column walks `zchunk` planes and
+// keeps the next plane's 19/27 pulled values in flight (register double
+// buffer) while it collides and stores the current one, so HBM sees a
+// continuous stream of loads instead of load/compute phases.  Cell masks are
+// prefetched two planes ahead so the pull addresses never wait on them.
+// Same per-cell arithmetic as k_fused: results are bit-identical.
+template <int Q, typename Real, int MODEL, int FORCE>
+__global__ void __launch_bounds__(128, 3)
+    k_fused_zm(KGrid g, KParams p, const Real* __restrict__ src, Real* __restrict__ dst,
+               const uint32_t* __restrict__ cellmask, const uint32_t* __restrict__ typemask,
+               int z0, int z1, int zchunk) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int zb = z0 + blockIdx.z * zchunk;
+    const int ze = min(zb + zchunk, z1);
+    const int xw0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    const bool gxy = (g.wrap_x && (xw0 == 0 || xw0 + 32 >= g.nx)) ||
+                     (g.wrap_y && (y == 0 || y == g.ny - 1));
+    if (x >= g.nx || zb >= ze) return;
+    const int64_t mstride = (int64_t)g.ny * g.nx;
+    const uint32_t* mrow = cellmask + (int64_t)y * g.nx + x;
+    auto edge_z = [&](int z) {
+        return (g.zlo == LBM_ZFACE_WRAP && z == 0) || (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1);
+    };
+    uint32_t c0 = __ldg(mrow + zb * mstride);
+    uint32_t c1 = (zb + 1 < ze) ? __ldg(mrow + (zb + 1) * mstride) : 0u;
+    double fa[Q], fb[Q];
+    pull_cell<Q, Real>(g, p, src, x, y, zb, c0, typemask, gxy || edge_z(zb), fa);
+    for (int z = zb; z < ze; ++z) {
+        const uint32_t c2 = (z + 2 < ze) ? __ldg(mrow + (z + 2) * mstride) : 0u;
+        if (z + 1 < ze) pull_cell<Q, Real>(g, p, src, x, y, z + 1, c1, typemask,
+                                           gxy || edge_z(z + 1), fb);
+        if (c0 & LBM_MASK_FLUID) collide_cell<Q, MODEL, FORCE>(fa, p);
+        const int64_t own = lidx(g, z, 0, y, x);
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            Store<Real>::template store<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, fa[i]);
+        });
+#pragma unroll
+        for (int i = 0; i < Q; ++i) fa[i] = fb[i];
+        c0 = c1;
+        c1 = c2;
+    }
 }
 
 // G_0 = C(R_0): collide fluid interior cells in place.
