@@ -77,6 +77,7 @@ extern "C" {
 #define LBM_FORCE_NONE 0
 #define LBM_FORCE_GUO 1
 #define LBM_FORCE_SHIFT 2
+#define LBM_FORCE_GUO_X 3 /* Guo with F = (fx, 0, 0): same values, fewer flops */
 
 /* cell-mask bits written by lbm_build_cellmask */
 #define LBM_MASK_FLUID 0x1u        /* bit 0: cell is collided              */

@@ -59,25 +59,33 @@ def _run(cmd, log=None):
     return res
 
 
-def build_kernels(force: bool = False, verbose: bool = False) -> Path:
+def build_kernels(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Build the library.  `defines` / `out` produce tuning variants (e.g.
+    defines=("LBM_FUSED_MINB=5",), out=.../_lbm_b200_minb5.so) that
+    _lib.load() picks up through LBM_B200_LIB."""
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "lbm_b200.h"]
-    OBJ.mkdir(exist_ok=True)
+    tag = "".join("_" + d.replace("=", "").lower() for d in defines)
+    objdir = OBJ / ("default" if not tag else tag.strip("_"))
+    objdir.mkdir(parents=True, exist_ok=True)
+    lib = out or LIB
     nvcc = _nvcc()
     objs = []
-    with open(OBJ / "ptxas.log", "w") as log:
+    with open(objdir / "ptxas.log", "w") as log:
         for src, extra in UNITS:
             s = CSRC / src
-            o = OBJ / (Path(src).stem + ".o")
+            o = objdir / (Path(src).stem + ".o")
             objs.append(o)
             if force or _stale(o, [s, *headers]):
-                cmd = [nvcc, *ARCH, *NVCC_COMMON, *extra, "-I", str(ROOT / "include"),
-                       "-c", str(s), "-o", str(o)]
+                cmd = [nvcc, *ARCH, *NVCC_COMMON, *extra, *(f"-D{d}" for d in defines),
+                       "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
                 if verbose:
                     print(" ".join(cmd), flush=True)
                 _run(cmd, log)
-        if force or _stale(LIB, objs):
-            _run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"], log)
-    return LIB
+        if force or _stale(lib, objs):
+            _run([nvcc, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart"], log)
+    if not tag:
+        (OBJ / "ptxas.log").write_text((objdir / "ptxas.log").read_text())
+    return lib
 
 
 def build_oracle(force: bool = False) -> Path:

@@ -56,7 +56,8 @@ def load(path: Path | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    import os
+    p = Path(path or os.environ.get("LBM_B200_LIB") or LIB_PATH)
     if not p.exists():
         raise BackendError(
             f"B200 kernel library {p} is missing; build it with "

@@ -73,7 +73,7 @@ int check_grid(const lbm_grid_t* g, KGrid* k) {
 int check_params(const lbm_params_t* p, int q, KParams* k, cudaStream_t s, int real_bytes) {
     if (!p) return fail(LBM_EINVAL, "params is NULL");
     if (p->model < 0 || p->model > 2) return fail(LBM_EINVAL, "bad model %d", p->model);
-    if (p->force_mode < 0 || p->force_mode > 2)
+    if (p->force_mode < 0 || p->force_mode > 3)
         return fail(LBM_EINVAL, "bad force mode %d", p->force_mode);
     if (p->force_mode == LBM_FORCE_SHIFT && p->model != LBM_SRT)
         return fail(LBM_EINVAL, "SimpleShift needs an SRT model with one global rate");
@@ -372,7 +372,7 @@ int lbm_moments(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
     if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
     if (!src || !rho || !u || !bad_count) return fail(LBM_EINVAL, "NULL buffer");
     if (stream_form && (!cellmask || !typemask)) return fail(LBM_EINVAL, "NULL mask");
-    const int guo = p->force_mode == LBM_FORCE_GUO;
+    const int guo = p->force_mode == LBM_FORCE_GUO || p->force_mode == LBM_FORCE_GUO_X;
     cudaError_t e = g->real_bytes == 8 ? unit_f64::moments(g->q, guo, k, kp, src, cellmask, typemask,
                                                            stream_form, rho, u, bad_count, s)
                                        : unit_f32::moments(g->q, guo, k, kp, src, cellmask, typemask,
@@ -452,7 +452,7 @@ int lbm_collide_cells(int q, const lbm_params_t* p, double* f, int64_t n, void* 
     const unsigned blocks = (unsigned)((n + threads - 1) / threads);
     cudaError_t e = by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
-        const int m = p->model, fm = p->force_mode;
+        const int m = p->model, fm = p->force_mode == LBM_FORCE_GUO_X ? LBM_FORCE_GUO : p->force_mode;
         if (m == 0 && fm == 0) k_collide_cells<Q, 0, 0><<<blocks, threads, 0, s>>>(kp, f, n);
         else if (m == 0 && fm == 1) k_collide_cells<Q, 0, 1><<<blocks, threads, 0, s>>>(kp, f, n);
         else if (m == 0 && fm == 2) k_collide_cells<Q, 0, 2><<<blocks, threads, 0, s>>>(kp, f, n);
@@ -496,7 +496,7 @@ int lbm_macroscopic_cells(int q, const lbm_params_t* p, const double* f, double*
     if (!f || !rho || !u || !bad_count) return fail(LBM_EINVAL, "NULL buffer");
     const int threads = 128;
     const unsigned blocks = (unsigned)((n + threads - 1) / threads);
-    const int guo = p->force_mode == LBM_FORCE_GUO;
+    const int guo = p->force_mode == LBM_FORCE_GUO || p->force_mode == LBM_FORCE_GUO_X;
     cudaError_t e = by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         if (guo) k_macroscopic_cells<Q, 1><<<blocks, threads, 0, s>>>(kp, f, rho, u, bad_count, n);

@@ -102,21 +102,30 @@ __device__ __forceinline__ double guo_axis(double u, double cu3) {
     else return -u;
 }
 
-template <int Q, int I>
+// XONLY: force along x only (fy == fz == 0): the y/z terms of t are +-0 and
+// adding them leaves A fx unchanged, so dropping them is value-identical.
+template <int Q, int I, bool XONLY = false>
 __device__ __forceinline__ double guo_F(double ux, double uy, double uz, double cu,
                                         const KParams& p) {
     using D = Dirs<Q>;
     const double cu3 = 3.0 * cu;
-    const double t = (guo_axis<D::cx[I]>(ux, cu3) * p.fx + guo_axis<D::cy[I]>(uy, cu3) * p.fy) +
-                     guo_axis<D::cz[I]>(uz, cu3) * p.fz;
+    double t;
+    if constexpr (XONLY)
+        t = guo_axis<D::cx[I]>(ux, cu3) * p.fx;
+    else
+        t = (guo_axis<D::cx[I]>(ux, cu3) * p.fx + guo_axis<D::cy[I]>(uy, cu3) * p.fy) +
+            guo_axis<D::cz[I]>(uz, cu3) * p.fz;
     constexpr double w3 = 3.0 * D::w[I];
     return w3 * t;
 }
 
-// MODEL: 0 SRT, 1 TRT, 2 MRT.  FORCE: 0 none, 1 Guo, 2 SimpleShift.
+// MODEL: 0 SRT, 1 TRT, 2 MRT.  FORCE: 0 none, 1 Guo, 2 SimpleShift,
+// 3 Guo with the force along x only.
 template <int Q, int MODEL, int FORCE>
 __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
     using D = Dirs<Q>;
+    constexpr bool GUO = FORCE == 1 || FORCE == 3;
+    constexpr bool XO = FORCE == 3;
     // density: sequential sum (_core_py.py:91-93)
     double rho = f[0];
 #pragma unroll
@@ -151,7 +160,7 @@ __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
             const double feq =
                 (wt<Q, i>() * rho) * (((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - usq15);
             double v = feq + p.rem * (f[i] - feq);
-            if constexpr (FORCE == 1) v = v + p.hw * guo_F<Q, i>(ux, uy, uz, cu, p);
+            if constexpr (GUO) v = v + p.hw * guo_F<Q, i, XO>(ux, uy, uz, cu, p);
             f[i] = v;
         });
     } else if constexpr (MODEL == 1) {
@@ -166,8 +175,8 @@ __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
                 const double ep = 0.5 * (feq0 + feq0);
                 const double em = 0.5 * (feq0 - feq0);
                 double v = (f[0] - p.omega_e * (fp - ep)) - p.omega_o * (fm - em);
-                if constexpr (FORCE == 1) {
-                    const double F0 = guo_F<Q, 0>(ux, uy, uz, 0.0, p);
+                if constexpr (GUO) {
+                    const double F0 = guo_F<Q, 0, XO>(ux, uy, uz, 0.0, p);
                     v = (v + p.he_half * (F0 + F0)) + p.ho_half * (F0 - F0);
                 }
                 f[0] = v;
@@ -186,9 +195,9 @@ __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
                 const double B = p.omega_o * (fm - em);
                 double vi = (f[i] - A) - B;
                 double vj = (f[j] - A) + B;
-                if constexpr (FORCE == 1) {
-                    const double Fi = guo_F<Q, i>(ux, uy, uz, cu, p);
-                    const double Fj = guo_F<Q, j>(ux, uy, uz, -cu, p);
+                if constexpr (GUO) {
+                    const double Fi = guo_F<Q, i, XO>(ux, uy, uz, cu, p);
+                    const double Fj = guo_F<Q, j, XO>(ux, uy, uz, -cu, p);
                     const double P = p.he_half * (Fi + Fj);
                     const double Qd = p.ho_half * (Fi - Fj);
                     vi = (vi + P) + Qd;
@@ -219,10 +228,10 @@ __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
             m[a] = c_mrt_S[a] * (acc - acq);
         }
         double Fi[Q];
-        if constexpr (FORCE == 1) {
+        if constexpr (GUO) {
             static_for<0, Q>([&](auto I_) {
                 constexpr int i = decltype(I_)::value;
-                Fi[i] = guo_F<Q, i>(ux, uy, uz, cu_of<Q, i>(ux, uy, uz), p);
+                Fi[i] = guo_F<Q, i, XO>(ux, uy, uz, cu_of<Q, i>(ux, uy, uz), p);
             });
         }
 #pragma unroll
@@ -232,7 +241,7 @@ __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
             for (int a = 1; a < Q; ++a) acc = acc + c_mrt_Minv[i * Q + a] * m[a];
             f[i] = f[i] - acc;
         }
-        if constexpr (FORCE == 1) {
+        if constexpr (GUO) {
 #pragma unroll
             for (int i = 0; i < Q; ++i) {
                 double acc = c_mrt_G[i * Q] * Fi[0];

@@ -18,33 +18,14 @@ inline dim3 cell_block(int nx) {
     return dim3(bx, 1, 1);
 }
 
-// z-chunk of the z-marching kernel; 0 selects the one-plane-per-block kernel.
-// LBM_ZCHUNK overrides (tuning runs).
-inline int zchunk_for(int planes) {
-    static int env = -2;
-    if (env == -2) {
-        const char* e = getenv("LBM_ZCHUNK");
-        env = e ? atoi(e) : -1;
-    }
-    if (env >= 0) return env;
-    return planes >= 8 ? 16 : 0;
-}
-
 template <int Q, int MODEL, int FORCE>
 cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst,
                     const uint32_t* cm, const uint32_t* tmk, int z0, int z1, cudaStream_t s) {
     if (z1 <= z0) return cudaSuccess;
     dim3 b = cell_block(g.nx);
-    const int zc = zchunk_for(z1 - z0);
-    if (zc > 0) {
-        dim3 grid((g.nx + b.x - 1) / b.x, g.ny, (z1 - z0 + zc - 1) / zc);
-        k_fused_zm<Q, LBM_REAL, MODEL, FORCE><<<grid, b, 0, s>>>(
-            g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0, z1, zc);
-    } else {
-        dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
-        k_fused<Q, LBM_REAL, MODEL, FORCE><<<grid, b, 0, s>>>(g, p, (const LBM_REAL*)src,
-                                                             (LBM_REAL*)dst, cm, tmk, z0);
-    }
+    dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
+    k_fused<Q, LBM_REAL, MODEL, FORCE><<<grid, b, 0, s>>>(g, p, (const LBM_REAL*)src,
+                                                         (LBM_REAL*)dst, cm, tmk, z0);
     return cudaGetLastError();
 }
 
@@ -67,6 +48,9 @@ cudaError_t by_model(int model, int force, F&& fn) {
     if (model == 1 && force == 1) return fn(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
     if (model == 2 && force == 0) return fn(std::integral_constant<int, 2>{}, std::integral_constant<int, 0>{});
     if (model == 2 && force == 1) return fn(std::integral_constant<int, 2>{}, std::integral_constant<int, 1>{});
+    if (model == 0 && force == 3) return fn(std::integral_constant<int, 0>{}, std::integral_constant<int, 3>{});
+    if (model == 1 && force == 3) return fn(std::integral_constant<int, 1>{}, std::integral_constant<int, 3>{});
+    if (model == 2 && force == 3) return fn(std::integral_constant<int, 2>{}, std::integral_constant<int, 3>{});
     return cudaErrorInvalidValue;
 }
 

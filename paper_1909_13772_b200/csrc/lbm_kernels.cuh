@@ -210,8 +210,24 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
 }
 
 // Fused pull -> bounce-back -> collide over interior planes [z0, z0+gridDim.z).
+// Resident 128-thread blocks per SM requested from ptxas (caps registers at
+// 65536 / (128 * minb)).  The kernel is latency-bound on its 19/27 pulls, so
+// occupancy beats the few L1-resident spills it costs (measured on B200,
+// config 4 D3Q19 TRT fp64: minb 1 -> 83 %, 5 -> 89 %, 6 -> 91.9 %,
+// 7 -> 92.4 %, 8 -> 89.7 % of the HBM roofline).  MRT keeps all registers.
+// -DLBM_FUSED_MINB=n overrides for tuning builds.
+template <int Q, int MODEL>
+constexpr int fused_minb() {
+#ifdef LBM_FUSED_MINB
+    return LBM_FUSED_MINB;
+#else
+    return MODEL == 2 ? 1 : (Q == 9 ? 8 : (Q == 19 ? 6 : 4));
+#endif
+}
+
 template <int Q, typename Real, int MODEL, int FORCE>
-__global__ void __launch_bounds__(128) k_fused(KGrid g, KParams p, const Real* __restrict__ src,
+__global__ void __launch_bounds__(128, fused_minb<Q, MODEL>())
+    k_fused(KGrid g, KParams p, const Real* __restrict__ src,
                                                Real* __restrict__ dst,
                                                const uint32_t* __restrict__ cellmask,
                                                const uint32_t* __restrict__ typemask, int z0) {
@@ -235,51 +251,6 @@ __global__ void __launch_bounds__(128) k_fused(KGrid g, KParams p, const Real* _
         constexpr int i = decltype(I_)::value;
         Store<Real>::template store<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
     });
-}
-
-// z-marching variant: one thread per (x, y) column walks `zchunk` planes and
-// keeps the next plane's 19/27 pulled values in flight (register double
-// buffer) while it collides and stores the current one, so HBM sees a
-// continuous stream of loads instead of load/compute phases.  Cell masks are
-// prefetched two planes ahead so the pull addresses never wait on them.
-// Same per-cell arithmetic as k_fused: results are bit-identical.
-template <int Q, typename Real, int MODEL, int FORCE>
-__global__ void __launch_bounds__(128, 3)
-    k_fused_zm(KGrid g, KParams p, const Real* __restrict__ src, Real* __restrict__ dst,
-               const uint32_t* __restrict__ cellmask, const uint32_t* __restrict__ typemask,
-               int z0, int z1, int zchunk) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y;
-    const int zb = z0 + blockIdx.z * zchunk;
-    const int ze = min(zb + zchunk, z1);
-    const int xw0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-    const bool gxy = (g.wrap_x && (xw0 == 0 || xw0 + 32 >= g.nx)) ||
-                     (g.wrap_y && (y == 0 || y == g.ny - 1));
-    if (x >= g.nx || zb >= ze) return;
-    const int64_t mstride = (int64_t)g.ny * g.nx;
-    const uint32_t* mrow = cellmask + (int64_t)y * g.nx + x;
-    auto edge_z = [&](int z) {
-        return (g.zlo == LBM_ZFACE_WRAP && z == 0) || (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1);
-    };
-    uint32_t c0 = __ldg(mrow + zb * mstride);
-    uint32_t c1 = (zb + 1 < ze) ? __ldg(mrow + (zb + 1) * mstride) : 0u;
-    double fa[Q], fb[Q];
-    pull_cell<Q, Real>(g, p, src, x, y, zb, c0, typemask, gxy || edge_z(zb), fa);
-    for (int z = zb; z < ze; ++z) {
-        const uint32_t c2 = (z + 2 < ze) ? __ldg(mrow + (z + 2) * mstride) : 0u;
-        if (z + 1 < ze) pull_cell<Q, Real>(g, p, src, x, y, z + 1, c1, typemask,
-                                           gxy || edge_z(z + 1), fb);
-        if (c0 & LBM_MASK_FLUID) collide_cell<Q, MODEL, FORCE>(fa, p);
-        const int64_t own = lidx(g, z, 0, y, x);
-        static_for<0, Q>([&](auto I_) {
-            constexpr int i = decltype(I_)::value;
-            Store<Real>::template store<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, fa[i]);
-        });
-#pragma unroll
-        for (int i = 0; i < Q; ++i) fa[i] = fb[i];
-        c0 = c1;
-        c1 = c2;
-    }
 }
 
 // G_0 = C(R_0): collide fluid interior cells in place.

@@ -196,7 +196,15 @@ def kernel_params(stencil: Stencil, model, force=None, *, ubb_velocity=(0.0, 0.0
             p.fx, p.fy, p.fz = force.force
             p.shift_fx, p.shift_fy, p.shift_fz = (tau * v for v in force.force)
         elif isinstance(force, Guo):
-            p.force_mode = 1
+            fx, fy, fz = force.force
+            # Guo(0, 0, 0) is bitwise the unforced collision (test_lbm.py:239-248);
+            # a force along x alone drops the +-0 y/z source terms (value-identical)
+            if fx == 0.0 and fy == 0.0 and fz == 0.0:
+                p.force_mode = 0
+            elif fy == 0.0 and fz == 0.0:
+                p.force_mode = 3
+            else:
+                p.force_mode = 1
             p.fx, p.fy, p.fz = force.force
             p.shift_fx, p.shift_fy, p.shift_fz = (0.5 * v for v in force.force)
         else:

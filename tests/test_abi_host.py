@@ -166,7 +166,9 @@ def test_kernel_params_host_constants():
                          ubb_velocity=(0.05, 0.01, 0.0), reference_density=1.0)
     s = kp.struct
     we, wo = oracle.trt_magic(1.7)
-    assert s.model == 1 and s.force_mode == 1
+    assert s.model == 1 and s.force_mode == 3          # Guo along x only
+    assert P.kernel_params(st, P.SRT(1.2), P.Guo((0, 0, 0))).struct.force_mode == 0
+    assert P.kernel_params(st, P.SRT(1.2), P.Guo((1e-5, 1e-6, 0))).struct.force_mode == 1
     assert s.omega_e == we and s.omega_o == wo
     assert s.he_half == (1.0 - 0.5 * we) * 0.5 and s.ho_half == (1.0 - 0.5 * wo) * 0.5
     assert s.shift_fx == 0.5 * 1e-6
