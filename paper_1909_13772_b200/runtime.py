@@ -85,7 +85,9 @@ def init_distributed(backend: str | None = None) -> Context:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group(backend=backend)
+        import datetime
+        # fail instead of hanging forever if a peer dies mid-exchange
+        dist.init_process_group(backend=backend, timeout=datetime.timedelta(seconds=600))
     return Context()
 
 
