@@ -11,6 +11,7 @@ from __future__ import annotations
 import os
 import shutil
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 import sys
 from pathlib import Path
 
@@ -69,18 +70,22 @@ def build_kernels(force: bool = False, verbose: bool = False, defines=(), out: P
     objdir.mkdir(parents=True, exist_ok=True)
     lib = out or LIB
     nvcc = _nvcc()
-    objs = []
+    objs, cmds = [], []
+    for src, extra in UNITS:
+        s = CSRC / src
+        o = objdir / (Path(src).stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [s, *headers]):
+            cmds.append([nvcc, *ARCH, *NVCC_COMMON, *extra, *(f"-D{d}" for d in defines),
+                         "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)])
     with open(objdir / "ptxas.log", "w") as log:
-        for src, extra in UNITS:
-            s = CSRC / src
-            o = objdir / (Path(src).stem + ".o")
-            objs.append(o)
-            if force or _stale(o, [s, *headers]):
-                cmd = [nvcc, *ARCH, *NVCC_COMMON, *extra, *(f"-D{d}" for d in defines),
-                       "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
+        # the units are independent: compile them concurrently
+        with ThreadPoolExecutor(max_workers=len(UNITS)) as pool:
+            for cmd in cmds:
                 if verbose:
                     print(" ".join(cmd), flush=True)
-                _run(cmd, log)
+            for res in pool.map(_run, cmds):
+                log.write(res.args[-3] + "\n" + res.stdout + res.stderr + "\n")
         if force or _stale(lib, objs):
             _run([nvcc, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart"], log)
     if not tag:

@@ -92,11 +92,26 @@ int check_params(const lbm_params_t* p, int q, KParams* k, cudaStream_t s, int r
     for (int i = 0; i < 27; ++i) {
         k->ubb[i] = p->ubb[i];
         k->pw[i] = p->pressure[i];
+        k->fubb[i] = (float)p->ubb[i];
     }
+    k->frem = (float)p->rem;
+    k->fhw = (float)p->hw;
+    k->fomega_e = (float)p->omega_e;
+    k->fomega_o = (float)p->omega_o;
+    k->fhe_half = (float)p->he_half;
+    k->fho_half = (float)p->ho_half;
+    k->ffx = (float)p->fx;
+    k->ffy = (float)p->fy;
+    k->ffz = (float)p->fz;
+    k->fsfx = (float)p->shift_fx;
+    k->fsfy = (float)p->shift_fy;
+    k->fsfz = (float)p->shift_fz;
+    k->mrt_fast = 0;
     if (p->model == LBM_MRT) {
         if (!p->mrt) return fail(LBM_EINVAL, "MRT needs its tables");
         cudaError_t e = real_bytes == 8 ? set_mrt_tables_f64(q, p->mrt, s)
                                         : set_mrt_tables_f32(q, p->mrt, s);
+        if (e == cudaSuccess && real_bytes == 4) e = set_mrt_fast_f32(q, p->mrt, s, &k->mrt_fast);
         if (e != cudaSuccess) return cuda_status(e, "MRT tables");
     }
     return LBM_OK;

@@ -27,6 +27,11 @@ struct KParams {
     double sfx, sfy, sfz;         // 0.5 F (Guo) or tau F (SimpleShift)
     double ubb[27];               // per link direction k
     double pw[27];                // (2 w_k) rho_w, Pressure links
+    // fp32-storage path: the same constants rounded once on the host
+    float frem, fhw, fomega_e, fomega_o, fhe_half, fho_half;
+    float ffx, ffy, ffz, fsfx, fsfy, fsfz;
+    float fubb[27];
+    int mrt_fast;                 // fp32 D3Q27 MRT: factorised raw-moment form
 };
 
 // MRT tables in constant memory: M, Minv, S, G (q <= 27).  One private copy
@@ -67,8 +72,8 @@ static __constant__ double c_mrt_G[LBM_MRT_MAXQ * LBM_MRT_MAXQ];
     }
 
 // term c * u for c in {-1, 0, 1}, appended to a left-assoc sum
-template <int C>
-__device__ __forceinline__ double add_cu(double acc, double u, bool& started) {
+template <int C, typename T>
+__device__ __forceinline__ T add_cu(T acc, T u, bool& started) {
     if constexpr (C == 1) {
         if (started) return acc + u;
         started = true;
@@ -83,11 +88,11 @@ __device__ __forceinline__ double add_cu(double acc, double u, bool& started) {
 }
 
 // cu_i = (cx ux + cy uy) + cz uz with zero terms dropped (_core_py.py:127)
-template <int Q, int I>
-__device__ __forceinline__ double cu_of(double ux, double uy, double uz) {
+template <int Q, int I, typename T = double>
+__device__ __forceinline__ T cu_of(T ux, T uy, T uz) {
     using D = Dirs<Q>;
     bool started = false;
-    double acc = 0.0;
+    T acc = T(0);
     acc = add_cu<D::cx[I]>(acc, ux, started);
     acc = add_cu<D::cy[I]>(acc, uy, started);
     acc = add_cu<D::cz[I]>(acc, uz, started);

@@ -1,0 +1,230 @@
+// Per-cell collision of the fp32-storage path, fp32 registers.
+//
+// The fp32 field stores zero-centred populations g_i = f_i - w_i (SURVEY
+// hard part 8).  This path keeps them centred through the collision, so
+// every fp32 rounding error is relative to |f - w| (~1e-2 w) instead of |f|:
+//   drho = sum g_i,   rho = 1 + drho,   j = sum c_i g_i   (sum c_i w_i = 0)
+//   g_i^eq = w_i drho + (w_i rho) ((3 cu + 4.5 cu^2) - 1.5 u^2)
+// which is feq_i - w_i of impl.collide (_core_py.py:124-128) regrouped.
+// SRT/TRT/Guo follow _core_py.py:130-148,171-190 (w_i = w_opp(i), so the TRT
+// pair algebra is unchanged in g).  Results are checked against the fp64
+// oracle at BASELINE's 1e-5 relative tolerance, not bitwise, so sums are
+// reassociated for ILP and FMA contraction is allowed.
+//
+// D3Q27 MRT uses the raw-moment factorisation instead of the dense q x q
+// products of _core_py.py:149-169 / :191-197:
+//   f' = f - Minv S M (f - feq) + G F,  G = Minv (I - S/2) M
+//      = f + F - Rinv K R (d + F/2),    d = f - feq,  K = R Minv S M Rinv
+// where R is the tensor-product raw-moment transform (per axis: 1, c, c^2;
+// 3 passes of 9 three-point butterflies).  For bases that are raw monomials
+// up to a mixing of the second-order pure moments (the shear-separated basis
+// of BASELINE config 2), K is diagonal plus one 3x3 block on (xx, yy, zz);
+// the host checks that structure (set_mrt_fast_f32) before enabling it.
+#pragma once
+#include <type_traits>
+
+#include "lbm_collide.cuh"
+
+namespace lbm {
+
+static __constant__ float c_mrt_kd[27];  // K diagonal (raw index a + 3b + 9c)
+static __constant__ float c_mrt_kb[9];   // K on (xx, yy, zz) = raw 2, 6, 18
+
+constexpr int RAW_XX = 2, RAW_YY = 6, RAW_ZZ = 18;
+
+// tensor position of D3Q27 direction i: (cx+1) + 3 (cy+1) + 9 (cz+1)
+template <int I>
+constexpr int tpos27() {
+    return (Dirs<27>::cx[I] + 1) + 3 * (Dirs<27>::cy[I] + 1) + 9 * (Dirs<27>::cz[I] + 1);
+}
+
+// one axis of the raw transform: values at c = -1, 0, +1 -> moments c^0, c^1, c^2
+template <int STRIDE>
+__device__ __forceinline__ void raw_fwd_axis(float (&t)[27]) {
+    static_for<0, 27>([&](auto K_) {
+        constexpr int k = decltype(K_)::value;
+        if constexpr ((k / STRIDE) % 3 == 0) {
+            const float a = t[k], b = t[k + STRIDE], c = t[k + 2 * STRIDE];
+            t[k] = (a + c) + b;
+            t[k + STRIDE] = c - a;
+            t[k + 2 * STRIDE] = c + a;
+        }
+    });
+}
+
+template <int STRIDE>
+__device__ __forceinline__ void raw_inv_axis(float (&t)[27]) {
+    static_for<0, 27>([&](auto K_) {
+        constexpr int k = decltype(K_)::value;
+        if constexpr ((k / STRIDE) % 3 == 0) {
+            const float m0 = t[k], m1 = t[k + STRIDE], m2 = t[k + 2 * STRIDE];
+            t[k] = 0.5f * (m2 - m1);
+            t[k + STRIDE] = m0 - m2;
+            t[k + 2 * STRIDE] = 0.5f * (m2 + m1);
+        }
+    });
+}
+
+// (c - u + (3 cu) c) for one axis, fp32
+template <int C>
+__device__ __forceinline__ float guo_axis32(float u, float cu3) {
+    if constexpr (C == 1) return (1.0f - u) + cu3;
+    else if constexpr (C == -1) return (-1.0f - u) - cu3;
+    else return -u;
+}
+
+template <int Q, int I, bool XONLY>
+__device__ __forceinline__ float guo_F32(float ux, float uy, float uz, float cu,
+                                         const KParams& p) {
+    using D = Dirs<Q>;
+    const float cu3 = 3.0f * cu;
+    float t;
+    if constexpr (XONLY)
+        t = guo_axis32<D::cx[I]>(ux, cu3) * p.ffx;
+    else
+        t = (guo_axis32<D::cx[I]>(ux, cu3) * p.ffx + guo_axis32<D::cy[I]>(uy, cu3) * p.ffy) +
+            guo_axis32<D::cz[I]>(uz, cu3) * p.ffz;
+    constexpr float w3 = (float)(3.0 * D::w[I]);
+    return w3 * t;
+}
+
+template <int Q, int I>
+__device__ __forceinline__ constexpr float wtf() {
+    constexpr float v = (float)Dirs<Q>::w[I];
+    return v;
+}
+
+// MODEL: 0 SRT, 1 TRT, 2 MRT (dense, fp64 registers), 3 MRT factorised (Q=27).
+template <int Q, int MODEL, int FORCE>
+__device__ __forceinline__ void collide_cell_c32(float (&g)[Q], const KParams& p) {
+    using D = Dirs<Q>;
+    if constexpr (MODEL == 2) {
+        // dense tables: widen, run the fp64 restatement, re-centre
+        double f[Q];
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            f[i] = (double)g[i] + wt<Q, i>();
+        });
+        collide_cell<Q, 2, FORCE>(f, p);
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            g[i] = (float)(f[i] - wt<Q, i>());
+        });
+        return;
+    } else {
+        constexpr bool GUO = FORCE == 1 || FORCE == 3;
+        constexpr bool XO = FORCE == 3;
+        // density deviation and momentum: four / two partial sums for ILP
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+        float xp = 0.f, xm = 0.f, yp = 0.f, ym = 0.f, zp = 0.f, zm = 0.f;
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            s[i & 3] += g[i];
+            if constexpr (D::cx[i] == 1) xp += g[i];
+            if constexpr (D::cx[i] == -1) xm += g[i];
+            if constexpr (D::cy[i] == 1) yp += g[i];
+            if constexpr (D::cy[i] == -1) ym += g[i];
+            if constexpr (D::cz[i] == 1) zp += g[i];
+            if constexpr (D::cz[i] == -1) zm += g[i];
+        });
+        const float drho = (s[0] + s[1]) + (s[2] + s[3]);
+        const float rho = 1.0f + drho;
+        const float inv = 1.0f / rho;
+        float ux = (xp - xm) * inv;
+        float uy = (yp - ym) * inv;
+        float uz = (zp - zm) * inv;
+        if constexpr (FORCE != 0) {
+            ux = fmaf(p.fsfx, inv, ux);
+            uy = fmaf(p.fsfy, inv, uy);
+            uz = fmaf(p.fsfz, inv, uz);
+        }
+        const float usq15 = 1.5f * ((ux * ux + uy * uy) + uz * uz);
+
+        if constexpr (MODEL == 0) {
+            static_for<0, Q>([&](auto I_) {
+                constexpr int i = decltype(I_)::value;
+                const float cu = cu_of<Q, i, float>(ux, uy, uz);
+                const float X = fmaf(4.5f * cu, cu, 3.0f * cu) - usq15;
+                const float geq = fmaf(wtf<Q, i>() * rho, X, wtf<Q, i>() * drho);
+                float v = fmaf(p.frem, g[i] - geq, geq);
+                if constexpr (GUO) v = fmaf(p.fhw, guo_F32<Q, i, XO>(ux, uy, uz, cu, p), v);
+                g[i] = v;
+            });
+        } else if constexpr (MODEL == 1) {
+            static_for<0, Q>([&](auto I_) {
+                constexpr int i = decltype(I_)::value;
+                constexpr int j = D::opp[i];
+                if constexpr (i == 0) {
+                    // f+ = f, f- = 0: relaxation of the rest population by omega_e
+                    const float geq0 = fmaf(wtf<Q, 0>() * rho, -usq15, wtf<Q, 0>() * drho);
+                    float v = g[0] - p.fomega_e * (g[0] - geq0);
+                    if constexpr (GUO) {
+                        const float F0 = guo_F32<Q, 0, XO>(ux, uy, uz, 0.0f, p);
+                        v = fmaf(2.0f * p.fhe_half, F0, v);
+                    }
+                    g[0] = v;
+                } else if constexpr (i < j) {
+                    const float cu = cu_of<Q, i, float>(ux, uy, uz);
+                    const float wr = wtf<Q, i>() * rho;
+                    // g^eq+ = w drho + w rho (4.5 cu^2 - 1.5 u^2), g^eq- = w rho 3 cu
+                    const float ep = fmaf(wr, fmaf(4.5f * cu, cu, -usq15), wtf<Q, i>() * drho);
+                    const float em = wr * (3.0f * cu);
+                    const float fp = 0.5f * (g[i] + g[j]);
+                    const float fm = 0.5f * (g[i] - g[j]);
+                    const float A = p.fomega_e * (fp - ep);
+                    const float B = p.fomega_o * (fm - em);
+                    float vi = (g[i] - A) - B;
+                    float vj = (g[j] - A) + B;
+                    if constexpr (GUO) {
+                        const float Fi = guo_F32<Q, i, XO>(ux, uy, uz, cu, p);
+                        const float Fj = guo_F32<Q, j, XO>(ux, uy, uz, -cu, p);
+                        const float P = p.fhe_half * (Fi + Fj);
+                        const float Qd = p.fho_half * (Fi - Fj);
+                        vi = (vi + P) + Qd;
+                        vj = (vj + P) - Qd;
+                    }
+                    g[i] = vi;
+                    g[j] = vj;
+                }
+            });
+        } else {
+            static_assert(MODEL == 3 && Q == 27, "factorised MRT is D3Q27 only");
+            float t[27];
+            float Fs[GUO ? 27 : 1];
+            static_for<0, 27>([&](auto I_) {
+                constexpr int i = decltype(I_)::value;
+                const float cu = cu_of<27, i, float>(ux, uy, uz);
+                const float X = fmaf(4.5f * cu, cu, 3.0f * cu) - usq15;
+                const float geq = fmaf(wtf<27, i>() * rho, X, wtf<27, i>() * drho);
+                float d = g[i] - geq;
+                if constexpr (GUO) {
+                    Fs[i] = guo_F32<27, i, XO>(ux, uy, uz, cu, p);
+                    d = fmaf(0.5f, Fs[i], d);
+                }
+                t[tpos27<i>()] = d;
+            });
+            raw_fwd_axis<1>(t);
+            raw_fwd_axis<3>(t);
+            raw_fwd_axis<9>(t);
+            const float bx = t[RAW_XX], by = t[RAW_YY], bz = t[RAW_ZZ];
+            static_for<0, 27>([&](auto K_) {
+                constexpr int k = decltype(K_)::value;
+                if constexpr (k != RAW_XX && k != RAW_YY && k != RAW_ZZ) t[k] *= c_mrt_kd[k];
+            });
+            t[RAW_XX] = fmaf(c_mrt_kb[0], bx, fmaf(c_mrt_kb[1], by, c_mrt_kb[2] * bz));
+            t[RAW_YY] = fmaf(c_mrt_kb[3], bx, fmaf(c_mrt_kb[4], by, c_mrt_kb[5] * bz));
+            t[RAW_ZZ] = fmaf(c_mrt_kb[6], bx, fmaf(c_mrt_kb[7], by, c_mrt_kb[8] * bz));
+            raw_inv_axis<1>(t);
+            raw_inv_axis<3>(t);
+            raw_inv_axis<9>(t);
+            static_for<0, 27>([&](auto I_) {
+                constexpr int i = decltype(I_)::value;
+                float v = g[i] - t[tpos27<i>()];
+                if constexpr (GUO) v += Fs[i];
+                g[i] = v;
+            });
+        }
+    }
+}
+
+}  // namespace lbm

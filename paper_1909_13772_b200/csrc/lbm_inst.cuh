@@ -38,9 +38,15 @@ cudaError_t collide_t(const KGrid& g, const KParams& p, void* pdf, const uint32_
     return cudaGetLastError();
 }
 
-// (model, force) -> template; SimpleShift only with SRT (collision.py:431-435)
+// (model, force) -> template; SimpleShift only with SRT (collision.py:431-435).
+// Model 3 = MRT in the factorised raw-moment form (fp32 storage, D3Q27 only).
 template <int Q, class F>
 cudaError_t by_model(int model, int force, F&& fn) {
+    if constexpr (std::is_same_v<LBM_REAL, float> && Q == 27) {
+        if (model == 3 && force == 0) return fn(std::integral_constant<int, 3>{}, std::integral_constant<int, 0>{});
+        if (model == 3 && force == 1) return fn(std::integral_constant<int, 3>{}, std::integral_constant<int, 1>{});
+        if (model == 3 && force == 3) return fn(std::integral_constant<int, 3>{}, std::integral_constant<int, 3>{});
+    }
     if (model == 0 && force == 0) return fn(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
     if (model == 0 && force == 1) return fn(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
     if (model == 0 && force == 2) return fn(std::integral_constant<int, 0>{}, std::integral_constant<int, 2>{});
@@ -69,6 +75,7 @@ namespace LBM_UNIT {
 cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p, const void* src,
                   void* dst, const uint32_t* cm, const uint32_t* tmk, int z0, int z1,
                   cudaStream_t s) {
+    if (model == 2 && p.mrt_fast) model = 3;
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         return by_model<Q>(model, force, [&](auto Mc, auto Fc) {
@@ -80,6 +87,7 @@ cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p,
 
 cudaError_t collide_only(int q, int model, int force, const KGrid& g, const KParams& p, void* pdf,
                          const uint32_t* cm, cudaStream_t s) {
+    if (model == 2 && p.mrt_fast) model = 3;
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         return by_model<Q>(model, force, [&](auto Mc, auto Fc) {

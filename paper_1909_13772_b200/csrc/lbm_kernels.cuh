@@ -23,6 +23,7 @@
 
 #include "../../include/lbm_b200.h"
 #include "lbm_collide.cuh"
+#include "lbm_collide_f32.cuh"
 
 namespace lbm {
 
@@ -89,10 +90,10 @@ __device__ __forceinline__ int64_t lidx(const KGrid& g, int z, int slot, int y, 
 // (boundary.py:171-195): rho, u from the cell's own post-collision state
 // (sequential sums, u = m / rho), then
 //   R[x, i] = -G[x, k] + (2 w_k rho_w) ((1 + (4.5 cu) cu) - 1.5 usq),  k = opp(i).
-template <int Q, typename Real>
+template <int Q, typename Real, typename Acc>
 __device__ __forceinline__ void pressure_links(const KGrid& g, const KParams& p,
                                             const Real* __restrict__ src, int64_t own,
-                                            uint32_t pm, double (&f)[Q]) {
+                                            uint32_t pm, Acc (&f)[Q]) {
     using D = Dirs<Q>;
     double c[Q];
     static_for<0, Q>([&](auto I_) {
@@ -119,7 +120,9 @@ __device__ __forceinline__ void pressure_links(const KGrid& g, const KParams& p,
         constexpr int k = D::opp[i];
         if ((pm >> i) & 1u) {
             const double cu = cu_of<Q, k>(ux, uy, uz);
-            f[i] = -c[k] + p.pw[k] * ((1.0 + (4.5 * cu) * cu) - usq15);
+            const double v = -c[k] + p.pw[k] * ((1.0 + (4.5 * cu) * cu) - usq15);
+            if constexpr (std::is_same_v<Acc, double>) f[i] = v;
+            else f[i] = (float)(v - wt<Q, i>());  // fp32 path: centred
         }
     });
 }
@@ -168,11 +171,15 @@ __device__ __forceinline__ void pull_offsets(const KGrid& g, int x, int y, int z
 // Three phases so every load of a cell is in flight at once: (1) source
 // offsets with the link substitution folded in as a select, (2) all loads,
 // (3) conversion + the rare UBB / Pressure corrections under one branch.
-template <int Q, typename Real>
+// Acc = double: widened populations f (fp64 storage, or fp32 readout);
+// Acc = float (fp32 storage only): the stored centred g = f - w as is.
+template <int Q, typename Real, typename Acc>
 __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                                           const Real* __restrict__ src, int x, int y, int z,
                                           uint32_t code, const uint32_t* __restrict__ typemask,
-                                          bool generic, double (&f)[Q]) {
+                                          bool generic, Acc (&f)[Q]) {
+    static_assert(std::is_same_v<Acc, double> || std::is_same_v<Real, float>,
+                  "fp32 registers only for fp32 storage");
     using D = Dirs<Q>;
     const int64_t own = lidx(g, z, 0, y, x);
     int64_t off[Q];
@@ -195,17 +202,22 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
     });
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
-        f[i] = Store<Real>::template widen<Q, i>(raw[i]);
+        if constexpr (std::is_same_v<Acc, double>) f[i] = Store<Real>::template widen<Q, i>(raw[i]);
+        else f[i] = raw[i];
     });
     if (typed) {
         if (t.x) {
             static_for<1, Q>([&](auto I_) {
                 constexpr int i = decltype(I_)::value;
                 constexpr int k = D::opp[i];
-                if ((t.x >> i) & 1u) f[i] = f[i] - p.ubb[k];
+                if constexpr (std::is_same_v<Acc, double>) {
+                    if ((t.x >> i) & 1u) f[i] = f[i] - p.ubb[k];
+                } else {
+                    if ((t.x >> i) & 1u) f[i] = f[i] - p.fubb[k];
+                }
             });
         }
-        if (t.y) pressure_links<Q, Real>(g, p, src, own, t.y, f);
+        if (t.y) pressure_links<Q, Real, Acc>(g, p, src, own, t.y, f);
     }
 }
 
@@ -216,17 +228,50 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
 // config 4 D3Q19 TRT fp64: minb 1 -> 83 %, 5 -> 89 %, 6 -> 91.9 %,
 // 7 -> 92.4 %, 8 -> 89.7 % of the HBM roofline).  MRT keeps all registers.
 // -DLBM_FUSED_MINB=n overrides for tuning builds.
-template <int Q, int MODEL>
+template <int Q, typename Real, int MODEL>
 constexpr int fused_minb() {
-#ifdef LBM_FUSED_MINB
-    return LBM_FUSED_MINB;
+    if constexpr (std::is_same_v<Real, float>) {
+        if constexpr (MODEL == 3) {
+#ifdef LBM_FUSED_MINB_F32MRT
+            return LBM_FUSED_MINB_F32MRT;
 #else
-    return MODEL == 2 ? 1 : (Q == 9 ? 8 : (Q == 19 ? 6 : 4));
+            return 7;  // measured on B200 (config 2): 4 -> 68 %, 5 -> 69 %, 6 -> 74.5 %, 7 -> 75.6 %, 10 -> 45 %
 #endif
+        }
+#ifdef LBM_FUSED_MINB_F32
+        return LBM_FUSED_MINB_F32;
+#else
+        // D3Q19 config 4 fp32: 6 -> 74 %, 7 -> 76 %, 8 -> 80.8 %, 9 -> 82 %, 10 -> 69 %
+        return MODEL == 2 ? 1 : (Q == 9 ? 8 : (Q == 19 ? 9 : 6));
+#endif
+    } else {
+#ifdef LBM_FUSED_MINB
+        return LBM_FUSED_MINB;
+#else
+        return MODEL == 2 ? 1 : (Q == 9 ? 8 : (Q == 19 ? 6 : 4));
+#endif
+    }
+}
+
+// register type of the fused / collide-only kernels: fp32 storage computes in
+// fp32 on centred populations (lbm_collide_f32.cuh), fp64 bitwise otherwise
+template <typename Real>
+using AccOf = std::conditional_t<std::is_same_v<Real, float>, float, double>;
+
+template <int Q, int MODEL, int FORCE, typename Acc>
+__device__ __forceinline__ void collide_any(Acc (&f)[Q], const KParams& p) {
+    if constexpr (std::is_same_v<Acc, double>) collide_cell<Q, MODEL, FORCE>(f, p);
+    else collide_cell_c32<Q, MODEL, FORCE>(f, p);
+}
+
+template <int Q, int I, typename Real, typename Acc>
+__device__ __forceinline__ void store_any(Real* p, Acc v) {
+    if constexpr (std::is_same_v<Acc, double>) Store<Real>::template store<Q, I>(p, v);
+    else *p = v;  // already centred fp32
 }
 
 template <int Q, typename Real, int MODEL, int FORCE>
-__global__ void __launch_bounds__(128, fused_minb<Q, MODEL>())
+__global__ void __launch_bounds__(128, fused_minb<Q, Real, MODEL>())
     k_fused(KGrid g, KParams p, const Real* __restrict__ src,
                                                Real* __restrict__ dst,
                                                const uint32_t* __restrict__ cellmask,
@@ -243,13 +288,14 @@ __global__ void __launch_bounds__(128, fused_minb<Q, MODEL>())
     const bool generic = edge_x || edge_y || edge_z;
     if (x >= g.nx) return;
     const uint32_t code = __ldg(cellmask + ((int64_t)z * g.ny + y) * g.nx + x);
-    double f[Q];
-    pull_cell<Q, Real>(g, p, src, x, y, z, code, typemask, generic, f);
-    if (code & LBM_MASK_FLUID) collide_cell<Q, MODEL, FORCE>(f, p);
+    using Acc = AccOf<Real>;
+    Acc f[Q];
+    pull_cell<Q, Real, Acc>(g, p, src, x, y, z, code, typemask, generic, f);
+    if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p);
     const int64_t own = lidx(g, z, 0, y, x);
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
-        Store<Real>::template store<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
+        store_any<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
     });
 }
 
@@ -264,15 +310,19 @@ __global__ void __launch_bounds__(128) k_collide_only(KGrid g, KParams p, Real* 
     const uint32_t code = cellmask[((int64_t)z * g.ny + y) * g.nx + x];
     if (!(code & LBM_MASK_FLUID)) return;
     const int64_t own = lidx(g, z, 0, y, x);
-    double f[Q];
+    using Acc = AccOf<Real>;
+    Acc f[Q];
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
-        f[i] = Store<Real>::template load<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane);
+        if constexpr (std::is_same_v<Acc, double>)
+            f[i] = Store<Real>::template load<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane);
+        else
+            f[i] = pdf[own + (int64_t)slot_of<Q>(i) * g.plane];
     });
-    collide_cell<Q, MODEL, FORCE>(f, p);
+    collide_any<Q, MODEL, FORCE>(f, p);
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
-        Store<Real>::template store<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
+        store_any<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
     });
 }
 
@@ -289,7 +339,7 @@ __global__ void __launch_bounds__(128) k_stream_only(KGrid g, KParams p, const R
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
     const uint32_t code = cellmask[cell];
     double f[Q];
-    pull_cell<Q, Real>(g, p, src, x, y, z, code, typemask, true, f);
+    pull_cell<Q, Real, double>(g, p, src, x, y, z, code, typemask, true, f);
     const int64_t n = (int64_t)g.nx * g.ny * g.nz;
 #pragma unroll
     for (int i = 0; i < Q; ++i) out[(int64_t)i * n + cell] = f[i];
@@ -310,7 +360,7 @@ __global__ void __launch_bounds__(128) k_moments(KGrid g, KParams p, const Real*
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
     double f[Q];
     if (stream_form) {
-        pull_cell<Q, Real>(g, p, src, x, y, z, cellmask[cell], typemask, true, f);
+        pull_cell<Q, Real, double>(g, p, src, x, y, z, cellmask[cell], typemask, true, f);
     } else {
         const int64_t own = lidx(g, z, 0, y, x);
         static_for<0, Q>([&](auto I_) {

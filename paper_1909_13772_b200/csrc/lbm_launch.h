@@ -34,4 +34,7 @@ LBM_DECLARE_UNIT(unit_f32)
 cudaError_t set_mrt_tables_f64(int q, const double* tables, cudaStream_t s);
 cudaError_t set_mrt_tables_f32(int q, const double* tables, cudaStream_t s);
 cudaError_t set_mrt_tables_capi(int q, const double* tables, cudaStream_t s);
+// fp32 unit: derive K = R Minv S M Rinv (raw-moment space) and enable the
+// factorised D3Q27 MRT when K has the supported structure (*fast = 1)
+cudaError_t set_mrt_fast_f32(int q, const double* tables, cudaStream_t s, int* fast);
 }  // namespace lbm
