@@ -67,6 +67,24 @@ int check_grid(const lbm_grid_t* g, KGrid* k) {
     k->zhi = g->zface_hi;
     k->plane = (int64_t)(g->ny + 2) * g->pitch;
     k->zstride = (int64_t)g->q * k->plane;
+    if ((int64_t)(g->q + 2) * k->plane >= ((int64_t)1 << 31))
+        return fail(LBM_EINVAL, "x-y plane of %lld elements too large for 32-bit in-plane offsets",
+                    (long long)k->plane);
+    k->plane32 = (int)k->plane;
+    k->zstride32 = (int)k->zstride;
+    auto fill = [&](auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        using D = Dirs<Q>;
+        for (int i = 0; i < 27; ++i) k->dpull[i] = k->dlink[i] = k->dslot[i] = 0;
+        for (int i = 0; i < Q; ++i) {
+            k->dslot[i] = slot_of<Q>(i) * k->plane32;
+            k->dpull[i] = k->dslot[i] - D::cz[i] * k->zstride32 - D::cy[i] * g->pitch - D::cx[i];
+            k->dlink[i] = slot_of<Q>(D::opp[i]) * k->plane32;
+        }
+    };
+    if (g->q == 9) fill(std::integral_constant<int, 9>{});
+    else if (g->q == 19) fill(std::integral_constant<int, 19>{});
+    else fill(std::integral_constant<int, 27>{});
     return LBM_OK;
 }
 
@@ -106,6 +124,18 @@ int check_params(const lbm_params_t* p, int q, KParams* k, cudaStream_t s, int r
     k->fsfx = (float)p->shift_fx;
     k->fsfy = (float)p->shift_fy;
     k->fsfz = (float)p->shift_fz;
+    for (int i = 0; i < 27; ++i) k->fcF[i] = k->fguo_p[i] = k->fguo_q[i] = 0.f;
+    for (int i = 0; i < q; ++i) {
+        int cx, cy, cz;
+        double w;
+        if (q == 9) { cx = Dirs<9>::cx[i]; cy = Dirs<9>::cy[i]; cz = Dirs<9>::cz[i]; w = Dirs<9>::w[i]; }
+        else if (q == 19) { cx = Dirs<19>::cx[i]; cy = Dirs<19>::cy[i]; cz = Dirs<19>::cz[i]; w = Dirs<19>::w[i]; }
+        else { cx = Dirs<27>::cx[i]; cy = Dirs<27>::cy[i]; cz = Dirs<27>::cz[i]; w = Dirs<27>::w[i]; }
+        const double cF = cx * p->fx + cy * p->fy + cz * p->fz;
+        k->fcF[i] = (float)cF;
+        k->fguo_p[i] = (float)(p->he_half * 6.0 * w);
+        k->fguo_q[i] = (float)(p->ho_half * 6.0 * w * cF);
+    }
     k->mrt_fast = 0;
     if (p->model == LBM_MRT) {
         if (!p->mrt) return fail(LBM_EINVAL, "MRT needs its tables");

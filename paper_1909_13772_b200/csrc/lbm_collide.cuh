@@ -31,6 +31,9 @@ struct KParams {
     float frem, fhw, fomega_e, fomega_o, fhe_half, fho_half;
     float ffx, ffy, ffz, fsfx, fsfy, fsfz;
     float fubb[27];
+    // fp32 TRT Guo pair constants: fcF = c_i . F, fguo_p = he_half 6 w_i
+    // (fguo_p[0] = 2 he_half 3 w_0), fguo_q = ho_half 6 w_i (c_i . F)
+    float fcF[27], fguo_p[27], fguo_q[27];
     int mrt_fast;                 // fp32 D3Q27 MRT: factorised raw-moment form
 };
 

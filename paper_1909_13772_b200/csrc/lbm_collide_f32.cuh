@@ -114,25 +114,32 @@ __device__ __forceinline__ void collide_cell_c32(float (&g)[Q], const KParams& p
     } else {
         constexpr bool GUO = FORCE == 1 || FORCE == 3;
         constexpr bool XO = FORCE == 3;
-        // density deviation and momentum: four / two partial sums for ILP
-        float s[4] = {0.f, 0.f, 0.f, 0.f};
-        float xp = 0.f, xm = 0.f, yp = 0.f, ym = 0.f, zp = 0.f, zm = 0.f;
-        static_for<0, Q>([&](auto I_) {
+        // density deviation and momentum from the pair sums / differences of
+        // (i, opp(i)), i < opp(i): drho = g_0 + sum sp, j = sum c_i dm
+        float sp[Q], dm[Q];
+        float s[3] = {g[0], 0.f, 0.f};
+        float mx = 0.f, my = 0.f, mz = 0.f;
+        static_for<1, Q>([&](auto I_) {
             constexpr int i = decltype(I_)::value;
-            s[i & 3] += g[i];
-            if constexpr (D::cx[i] == 1) xp += g[i];
-            if constexpr (D::cx[i] == -1) xm += g[i];
-            if constexpr (D::cy[i] == 1) yp += g[i];
-            if constexpr (D::cy[i] == -1) ym += g[i];
-            if constexpr (D::cz[i] == 1) zp += g[i];
-            if constexpr (D::cz[i] == -1) zm += g[i];
+            constexpr int j = D::opp[i];
+            if constexpr (i < j) {
+                sp[i] = g[i] + g[j];
+                dm[i] = g[i] - g[j];
+                s[i % 3] += sp[i];
+                if constexpr (D::cx[i] == 1) mx += dm[i];
+                if constexpr (D::cx[i] == -1) mx -= dm[i];
+                if constexpr (D::cy[i] == 1) my += dm[i];
+                if constexpr (D::cy[i] == -1) my -= dm[i];
+                if constexpr (D::cz[i] == 1) mz += dm[i];
+                if constexpr (D::cz[i] == -1) mz -= dm[i];
+            }
         });
-        const float drho = (s[0] + s[1]) + (s[2] + s[3]);
+        const float drho = (s[0] + s[1]) + s[2];
         const float rho = 1.0f + drho;
         const float inv = 1.0f / rho;
-        float ux = (xp - xm) * inv;
-        float uy = (yp - ym) * inv;
-        float uz = (zp - zm) * inv;
+        float ux = mx * inv;
+        float uy = my * inv;
+        float uz = mz * inv;
         if constexpr (FORCE != 0) {
             ux = fmaf(p.fsfx, inv, ux);
             uy = fmaf(p.fsfy, inv, uy);
@@ -151,40 +158,37 @@ __device__ __forceinline__ void collide_cell_c32(float (&g)[Q], const KParams& p
                 g[i] = v;
             });
         } else if constexpr (MODEL == 1) {
+            // TRT on pair sums s = g_i + g_j and differences d = g_i - g_j:
+            //   g_i' = g_i + X + Y,  g_j' = g_j + X - Y,
+            //   X = P - omega_e (s/2 - g^eq+),  Y = Qd - omega_o (d/2 - g^eq-)
+            // with the Guo pair terms P = he_half (F_i + F_j) = he6w (3 cu (c.F) - u.F)
+            // and Qd = ho_half (F_i - F_j) = ho6w (c.F), a per-direction constant.
+            float uF = 0.f;
+            if constexpr (GUO) {
+                if constexpr (XO) uF = ux * p.ffx;
+                else uF = fmaf(ux, p.ffx, fmaf(uy, p.ffy, uz * p.ffz));
+            }
             static_for<0, Q>([&](auto I_) {
                 constexpr int i = decltype(I_)::value;
                 constexpr int j = D::opp[i];
                 if constexpr (i == 0) {
-                    // f+ = f, f- = 0: relaxation of the rest population by omega_e
                     const float geq0 = fmaf(wtf<Q, 0>() * rho, -usq15, wtf<Q, 0>() * drho);
-                    float v = g[0] - p.fomega_e * (g[0] - geq0);
-                    if constexpr (GUO) {
-                        const float F0 = guo_F32<Q, 0, XO>(ux, uy, uz, 0.0f, p);
-                        v = fmaf(2.0f * p.fhe_half, F0, v);
-                    }
+                    float v = fmaf(-p.fomega_e, g[0] - geq0, g[0]);
+                    if constexpr (GUO) v = fmaf(p.fguo_p[0], -uF, v);
                     g[0] = v;
                 } else if constexpr (i < j) {
                     const float cu = cu_of<Q, i, float>(ux, uy, uz);
                     const float wr = wtf<Q, i>() * rho;
-                    // g^eq+ = w drho + w rho (4.5 cu^2 - 1.5 u^2), g^eq- = w rho 3 cu
                     const float ep = fmaf(wr, fmaf(4.5f * cu, cu, -usq15), wtf<Q, i>() * drho);
-                    const float em = wr * (3.0f * cu);
-                    const float fp = 0.5f * (g[i] + g[j]);
-                    const float fm = 0.5f * (g[i] - g[j]);
-                    const float A = p.fomega_e * (fp - ep);
-                    const float B = p.fomega_o * (fm - em);
-                    float vi = (g[i] - A) - B;
-                    float vj = (g[j] - A) + B;
+                    const float em = (3.0f * wr) * cu;
+                    float X = p.fomega_e * fmaf(-0.5f, sp[i], ep);
+                    float Y = p.fomega_o * fmaf(-0.5f, dm[i], em);
                     if constexpr (GUO) {
-                        const float Fi = guo_F32<Q, i, XO>(ux, uy, uz, cu, p);
-                        const float Fj = guo_F32<Q, j, XO>(ux, uy, uz, -cu, p);
-                        const float P = p.fhe_half * (Fi + Fj);
-                        const float Qd = p.fho_half * (Fi - Fj);
-                        vi = (vi + P) + Qd;
-                        vj = (vj + P) - Qd;
+                        X = fmaf(p.fguo_p[i], fmaf(3.0f * cu, p.fcF[i], -uF), X);
+                        Y = Y + p.fguo_q[i];
                     }
-                    g[i] = vi;
-                    g[j] = vj;
+                    g[i] = (g[i] + X) + Y;
+                    g[j] = (g[j] + X) - Y;
                 }
             });
         } else {

@@ -32,7 +32,20 @@ struct KGrid {
     int wrap_x, wrap_y, zlo, zhi;  // zlo/zhi: LBM_ZFACE_*
     int64_t plane;                 // (ny+2) * pitch
     int64_t zstride;               // q * plane
+    int plane32, zstride32;        // the same as int (the C-ABI checks (q+2) plane < 2^31)
+    // own-relative element deltas, indexed by reference direction i (host-computed):
+    int dpull[27];   // source of the pull of direction i: slot(i) plane - c_i . (1, pitch, zstride)
+    int dlink[27];   // bounce-back source: own cell, slot(opp(i)) plane
+    int dslot[27];   // slot(i) plane (stores)
 };
+
+// Opaque copy of a pointer: keeps `base + int32 delta` as one wide
+// multiply-add per access instead of a re-associated 64-bit index sum.
+template <typename T>
+__device__ __forceinline__ T* opaque(T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
 
 template <typename Real>
 struct Store;
@@ -182,24 +195,35 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                   "fp32 registers only for fp32 storage");
     using D = Dirs<Q>;
     const int64_t own = lidx(g, z, 0, y, x);
-    int64_t off[Q];
-    if (generic) pull_offsets<Q, true>(g, x, y, z, own, off);
-    else pull_offsets<Q, false>(g, x, y, z, own, off);
-    // link: read the own cell's direction k = opp(i) instead (w_k == w_i, so
-    // the fp32 zero-centring offset is the same)
-    static_for<1, Q>([&](auto I_) {
-        constexpr int i = decltype(I_)::value;
-        constexpr int ks = slot_of<Q>(D::opp[i]);
-        off[i] = ((code >> i) & 1u) ? own + (int64_t)ks * g.plane : off[i];
-    });
     const bool typed = (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) != 0u;
     uint2 t = make_uint2(0u, 0u);
     if (typed) t = __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
     Real raw[Q];
-    static_for<0, Q>([&](auto I_) {
-        constexpr int i = decltype(I_)::value;
-        raw[i] = __ldg(src + off[i]);
-    });
+    // link: read the own cell's direction k = opp(i) instead (w_k == w_i, so
+    // the fp32 zero-centring offset is the same)
+    if (!generic) {
+        // own-relative 32-bit element deltas: launch-uniform except for the
+        // link select, so each pull costs one select + one address multiply-add
+        const Real* sp = opaque(src + own);
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            int d = g.dpull[i];
+            if constexpr (i > 0) d = ((code >> i) & 1u) ? g.dlink[i] : d;
+            raw[i] = __ldg(sp + d);
+        });
+    } else {
+        int64_t off[Q];
+        pull_offsets<Q, true>(g, x, y, z, own, off);
+        static_for<1, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            constexpr int ks = slot_of<Q>(D::opp[i]);
+            off[i] = ((code >> i) & 1u) ? own + (int64_t)ks * g.plane : off[i];
+        });
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            raw[i] = __ldg(src + off[i]);
+        });
+    }
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
         if constexpr (std::is_same_v<Acc, double>) f[i] = Store<Real>::template widen<Q, i>(raw[i]);
@@ -292,10 +316,10 @@ __global__ void __launch_bounds__(128, fused_minb<Q, Real, MODEL>())
     Acc f[Q];
     pull_cell<Q, Real, Acc>(g, p, src, x, y, z, code, typemask, generic, f);
     if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p);
-    const int64_t own = lidx(g, z, 0, y, x);
+    Real* dp = opaque(dst + lidx(g, z, 0, y, x));
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
-        store_any<Q, i>(dst + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);
+        store_any<Q, i>(dp + g.dslot[i], f[i]);
     });
 }
 
