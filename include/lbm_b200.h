@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define LBM_B200_ABI_VERSION 1
+#define LBM_B200_ABI_VERSION 2
 
 /* status codes */
 #define LBM_OK 0
@@ -73,6 +73,10 @@ extern "C" {
 #define LBM_SRT 0
 #define LBM_TRT 1
 #define LBM_MRT 2
+/* SRT with a per-cell rate field (SRT(omega_field=key), lbm/sweep.py:111-146,
+ * _core_py.py:130-136): rem = 1 - omega(x), hw = 1 - 0.5 omega(x) per cell,
+ * omega(x) read from lbm_params_t.omega_cells */
+#define LBM_SRT_FIELD 3
 /* force models (Guo.mode / SimpleShift.mode, lbm/collision.py:115,128) */
 #define LBM_FORCE_NONE 0
 #define LBM_FORCE_GUO 1
@@ -118,6 +122,10 @@ typedef struct lbm_params {
      * 192-197): M[q*q], Minv[q*q], S[q], G[q*q] (G only for Guo).  NULL
      * unless model == LBM_MRT.                                          */
     const double* mrt;
+    /* LBM_SRT_FIELD: DEVICE pointer to the per-cell rates of this rank's box
+     * interior, (nz, ny, nx) fp64, same cell order as the cell mask.  NULL
+     * otherwise.  (ABI 2) */
+    const double* omega_cells;
 } lbm_params_t;
 
 /* ------------------------------------------------------------- metadata */

@@ -16,6 +16,8 @@ LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
 
 LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
 ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
+ABI_VERSION = 2
+SRT, TRT, MRT, SRT_FIELD = 0, 1, 2, 3
 MASK_FLUID = 0x1
 MASK_UBB = 0x80000000
 
@@ -45,7 +47,8 @@ class Params(ctypes.Structure):
                 ("fx", ctypes.c_double), ("fy", ctypes.c_double), ("fz", ctypes.c_double),
                 ("shift_fx", ctypes.c_double), ("shift_fy", ctypes.c_double),
                 ("shift_fz", ctypes.c_double), ("ubb", ctypes.c_double * 27),
-                ("pressure", ctypes.c_double * 27), ("mrt", ctypes.c_void_p)]
+                ("pressure", ctypes.c_double * 27), ("mrt", ctypes.c_void_p),
+                ("omega_cells", ctypes.c_void_p)]
 
 
 _lib = None
@@ -88,7 +91,7 @@ def load(path: Path | None = None):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.lbm_abi_version() != 1:
+    if lib.lbm_abi_version() != ABI_VERSION:
         raise BackendError("kernel library ABI mismatch")
     if (lib.lbm_struct_size(0) != ctypes.sizeof(Grid)
             or lib.lbm_struct_size(1) != ctypes.sizeof(Params)):

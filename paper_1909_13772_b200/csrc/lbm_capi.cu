@@ -90,7 +90,12 @@ int check_grid(const lbm_grid_t* g, KGrid* k) {
 
 int check_params(const lbm_params_t* p, int q, KParams* k, cudaStream_t s, int real_bytes) {
     if (!p) return fail(LBM_EINVAL, "params is NULL");
-    if (p->model < 0 || p->model > 2) return fail(LBM_EINVAL, "bad model %d", p->model);
+    if (p->model < 0 || p->model > 3) return fail(LBM_EINVAL, "bad model %d", p->model);
+    if (p->model == LBM_SRT_FIELD && !p->omega_cells)
+        return fail(LBM_EINVAL, "per-cell SRT rates need omega_cells");
+    if (p->model == LBM_SRT_FIELD && p->force_mode == LBM_FORCE_SHIFT)
+        return fail(LBM_EINVAL, "SimpleShift needs an SRT model with one global rate");
+    k->omega = p->omega_cells;
     if (p->force_mode < 0 || p->force_mode > 3)
         return fail(LBM_EINVAL, "bad force mode %d", p->force_mode);
     if (p->force_mode == LBM_FORCE_SHIFT && p->model != LBM_SRT)

@@ -35,6 +35,7 @@ struct KParams {
     // (fguo_p[0] = 2 he_half 3 w_0), fguo_q = ho_half 6 w_i (c_i . F)
     float fcF[27], fguo_p[27], fguo_q[27];
     int mrt_fast;                 // fp32 D3Q27 MRT: factorised raw-moment form
+    const double* omega;          // SRT per-cell rates (nz, ny, nx), model 4
 };
 
 // MRT tables in constant memory: M, Minv, S, G (q <= 27).  One private copy
@@ -127,10 +128,11 @@ __device__ __forceinline__ double guo_F(double ux, double uy, double uz, double 
     return w3 * t;
 }
 
-// MODEL: 0 SRT, 1 TRT, 2 MRT.  FORCE: 0 none, 1 Guo, 2 SimpleShift,
-// 3 Guo with the force along x only.
+// MODEL: 0 SRT, 1 TRT, 2 MRT, 4 SRT with the per-cell rate `om`
+// (rem = 1 - om, hw = 1 - 0.5 om as _core_py.py:133-134,181 compute them).
+// FORCE: 0 none, 1 Guo, 2 SimpleShift, 3 Guo with the force along x only.
 template <int Q, int MODEL, int FORCE>
-__device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
+__device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p, double om = 0.0) {
     using D = Dirs<Q>;
     constexpr bool GUO = FORCE == 1 || FORCE == 3;
     constexpr bool XO = FORCE == 3;
@@ -160,15 +162,17 @@ __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p) {
     }
     const double usq15 = 1.5 * ((ux * ux + uy * uy) + uz * uz);
 
-    if constexpr (MODEL == 0) {
+    if constexpr (MODEL == 0 || MODEL == 4) {
         // SRT (_core_py.py:130-136) + Guo source (:180-183)
+        const double rem = MODEL == 0 ? p.rem : 1.0 - om;
+        const double hw = MODEL == 0 ? p.hw : 1.0 - 0.5 * om;
         static_for<0, Q>([&](auto I_) {
             constexpr int i = decltype(I_)::value;
             const double cu = cu_of<Q, i>(ux, uy, uz);
             const double feq =
                 (wt<Q, i>() * rho) * (((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - usq15);
-            double v = feq + p.rem * (f[i] - feq);
-            if constexpr (GUO) v = v + p.hw * guo_F<Q, i, XO>(ux, uy, uz, cu, p);
+            double v = feq + rem * (f[i] - feq);
+            if constexpr (GUO) v = v + hw * guo_F<Q, i, XO>(ux, uy, uz, cu, p);
             f[i] = v;
         });
     } else if constexpr (MODEL == 1) {

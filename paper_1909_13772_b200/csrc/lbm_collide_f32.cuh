@@ -94,9 +94,10 @@ __device__ __forceinline__ constexpr float wtf() {
     return v;
 }
 
-// MODEL: 0 SRT, 1 TRT, 2 MRT (dense, fp64 registers), 3 MRT factorised (Q=27).
+// MODEL: 0 SRT, 1 TRT, 2 MRT (dense, fp64 registers), 3 MRT factorised (Q=27),
+// 4 SRT with the per-cell rate `om`.
 template <int Q, int MODEL, int FORCE>
-__device__ __forceinline__ void collide_cell_c32(float (&g)[Q], const KParams& p) {
+__device__ __forceinline__ void collide_cell_c32(float (&g)[Q], const KParams& p, double om = 0.0) {
     using D = Dirs<Q>;
     if constexpr (MODEL == 2) {
         // dense tables: widen, run the fp64 restatement, re-centre
@@ -147,14 +148,16 @@ __device__ __forceinline__ void collide_cell_c32(float (&g)[Q], const KParams& p
         }
         const float usq15 = 1.5f * ((ux * ux + uy * uy) + uz * uz);
 
-        if constexpr (MODEL == 0) {
+        if constexpr (MODEL == 0 || MODEL == 4) {
+            const float rem = MODEL == 0 ? p.frem : (float)(1.0 - om);
+            const float hw = MODEL == 0 ? p.fhw : (float)(1.0 - 0.5 * om);
             static_for<0, Q>([&](auto I_) {
                 constexpr int i = decltype(I_)::value;
                 const float cu = cu_of<Q, i, float>(ux, uy, uz);
                 const float X = fmaf(4.5f * cu, cu, 3.0f * cu) - usq15;
                 const float geq = fmaf(wtf<Q, i>() * rho, X, wtf<Q, i>() * drho);
-                float v = fmaf(p.frem, g[i] - geq, geq);
-                if constexpr (GUO) v = fmaf(p.fhw, guo_F32<Q, i, XO>(ux, uy, uz, cu, p), v);
+                float v = fmaf(rem, g[i] - geq, geq);
+                if constexpr (GUO) v = fmaf(hw, guo_F32<Q, i, XO>(ux, uy, uz, cu, p), v);
                 g[i] = v;
             });
         } else if constexpr (MODEL == 1) {

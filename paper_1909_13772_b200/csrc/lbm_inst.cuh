@@ -47,6 +47,10 @@ cudaError_t by_model(int model, int force, F&& fn) {
         if (model == 3 && force == 1) return fn(std::integral_constant<int, 3>{}, std::integral_constant<int, 1>{});
         if (model == 3 && force == 3) return fn(std::integral_constant<int, 3>{}, std::integral_constant<int, 3>{});
     }
+    // ABI model 3 (SRT with a per-cell rate field) is kernel model 4
+    if (model == 4 && force == 0) return fn(std::integral_constant<int, 4>{}, std::integral_constant<int, 0>{});
+    if (model == 4 && force == 1) return fn(std::integral_constant<int, 4>{}, std::integral_constant<int, 1>{});
+    if (model == 4 && force == 3) return fn(std::integral_constant<int, 4>{}, std::integral_constant<int, 3>{});
     if (model == 0 && force == 0) return fn(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{});
     if (model == 0 && force == 1) return fn(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
     if (model == 0 && force == 2) return fn(std::integral_constant<int, 0>{}, std::integral_constant<int, 2>{});
@@ -75,7 +79,8 @@ namespace LBM_UNIT {
 cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p, const void* src,
                   void* dst, const uint32_t* cm, const uint32_t* tmk, int z0, int z1,
                   cudaStream_t s) {
-    if (model == 2 && p.mrt_fast) model = 3;
+    if (model == LBM_SRT_FIELD) model = 4;
+    else if (model == LBM_MRT && p.mrt_fast) model = 3;
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         return by_model<Q>(model, force, [&](auto Mc, auto Fc) {
@@ -87,7 +92,8 @@ cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p,
 
 cudaError_t collide_only(int q, int model, int force, const KGrid& g, const KParams& p, void* pdf,
                          const uint32_t* cm, cudaStream_t s) {
-    if (model == 2 && p.mrt_fast) model = 3;
+    if (model == LBM_SRT_FIELD) model = 4;
+    else if (model == LBM_MRT && p.mrt_fast) model = 3;
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         return by_model<Q>(model, force, [&](auto Mc, auto Fc) {

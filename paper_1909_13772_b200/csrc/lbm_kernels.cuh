@@ -283,9 +283,11 @@ template <typename Real>
 using AccOf = std::conditional_t<std::is_same_v<Real, float>, float, double>;
 
 template <int Q, int MODEL, int FORCE, typename Acc>
-__device__ __forceinline__ void collide_any(Acc (&f)[Q], const KParams& p) {
-    if constexpr (std::is_same_v<Acc, double>) collide_cell<Q, MODEL, FORCE>(f, p);
-    else collide_cell_c32<Q, MODEL, FORCE>(f, p);
+__device__ __forceinline__ void collide_any(Acc (&f)[Q], const KParams& p, int64_t cell) {
+    double om = 0.0;
+    if constexpr (MODEL == 4) om = __ldg(p.omega + cell);
+    if constexpr (std::is_same_v<Acc, double>) collide_cell<Q, MODEL, FORCE>(f, p, om);
+    else collide_cell_c32<Q, MODEL, FORCE>(f, p, om);
 }
 
 template <int Q, int I, typename Real, typename Acc>
@@ -311,11 +313,12 @@ __global__ void __launch_bounds__(128, fused_minb<Q, Real, MODEL>())
     const bool edge_z = (g.zlo == LBM_ZFACE_WRAP && z == 0) || (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1);
     const bool generic = edge_x || edge_y || edge_z;
     if (x >= g.nx) return;
-    const uint32_t code = __ldg(cellmask + ((int64_t)z * g.ny + y) * g.nx + x);
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    const uint32_t code = __ldg(cellmask + cell);
     using Acc = AccOf<Real>;
     Acc f[Q];
     pull_cell<Q, Real, Acc>(g, p, src, x, y, z, code, typemask, generic, f);
-    if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p);
+    if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p, cell);
     Real* dp = opaque(dst + lidx(g, z, 0, y, x));
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
@@ -331,7 +334,8 @@ __global__ void __launch_bounds__(128) k_collide_only(KGrid g, KParams p, Real* 
     const int y = blockIdx.y;
     const int z = blockIdx.z;
     if (x >= g.nx) return;
-    const uint32_t code = cellmask[((int64_t)z * g.ny + y) * g.nx + x];
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    const uint32_t code = cellmask[cell];
     if (!(code & LBM_MASK_FLUID)) return;
     const int64_t own = lidx(g, z, 0, y, x);
     using Acc = AccOf<Real>;
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(128) k_collide_only(KGrid g, KParams p, Real* 
         else
             f[i] = pdf[own + (int64_t)slot_of<Q>(i) * g.plane];
     });
-    collide_any<Q, MODEL, FORCE>(f, p);
+    collide_any<Q, MODEL, FORCE>(f, p, cell);
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
         store_any<Q, i>(pdf + own + (int64_t)slot_of<Q>(i) * g.plane, f[i]);

@@ -183,6 +183,7 @@ class DeviceLattice:
         self._halo = None
         self._streams = None
         self._fluid_masks = None
+        self._rates = None        # (host copy, device tensor, version) of per-cell SRT rates
 
     # ---------------------------------------------------------- plumbing
     @property
@@ -201,6 +202,20 @@ class DeviceLattice:
         return [b.data[key].view_nosync for b in self.box.blocks]
 
     # ------------------------------------------------------ host <-> HBM
+    def set_rates(self, dense) -> int:
+        """Per-cell SRT rates (nz, ny, nx) fp64 -> HBM; returns a version
+        number that changes only when the values do."""
+        if self._rates is not None and np.array_equal(self._rates[0], dense):
+            return self._rates[2]
+        version = 0 if self._rates is None else self._rates[2] + 1
+        t = torch.from_numpy(dense).to(self.device)
+        self._rates = (dense.copy(), t, version)
+        return version
+
+    @property
+    def omega_ptr(self):
+        return self._rates[1].data_ptr()
+
     def upload_host(self):
         """Host R-form (src slot, ghosts incl.) -> buffer[cur] (kind R)."""
         fields = [b.data[self.pdf.key] for b in self.box.blocks]

@@ -172,12 +172,14 @@ def kernel_params(stencil: Stencil, model, force=None, *, ubb_velocity=(0.0, 0.0
     tables = None
     if isinstance(model, SRT):
         if model.omega is None:
-            raise ValidationError("per-cell SRT rates (omega_field) are not supported on the "
-                                  "B200 path yet")
-        p.model = 0
-        p.omega = model.omega
-        p.rem = 1.0 - model.omega
-        p.hw = 1.0 - 0.5 * model.omega
+            # per-cell rates: the sweep points omega_cells at the device copy
+            # of the rate field (lbm/sweep.py:111-146)
+            p.model = _lib.SRT_FIELD
+        else:
+            p.model = 0
+            p.omega = model.omega
+            p.rem = 1.0 - model.omega
+            p.hw = 1.0 - 0.5 * model.omega
     elif isinstance(model, TRT):
         p.model = 1
         p.omega_e, p.omega_o = model.omega_e, model.omega_o

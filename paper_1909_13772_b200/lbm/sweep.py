@@ -94,7 +94,8 @@ class PdfField:
             for k in range(self.stencil.q):
                 kp.struct.pressure[k] = 2.0 * self.stencil.weights[k] * handling.pressure_density
         s = kp.struct
-        key = (bytes(memoryview(s))[:-8], b"" if kp.tables is None else kp.tables.tobytes())
+        # (struct minus its two trailing pointers, MRT tables)
+        key = (bytes(memoryview(s))[:-16], b"" if kp.tables is None else kp.tables.tobytes())
         # keep the objects alive so their ids cannot be reused
         self._kp_cache[ck] = ((model, force, handling), kp, key)
         return kp, key
@@ -205,8 +206,6 @@ def _prepare(pdf: PdfField, model, force, handling):
         handling.freeze()
     if pdf.g != 1:
         raise ValidationError("stream-collide needs exactly one pdf ghost layer")
-    if getattr(model, "omega_field", None) is not None:
-        raise ValidationError("per-cell SRT rates (omega_field) are not supported on the B200 path yet")
     lat = pdf.lattice
     if handling is not None:
         for block in forest.local_blocks():
@@ -220,9 +219,30 @@ def _prepare(pdf: PdfField, model, force, handling):
         masks = lat.default_masks()
     kp, key = pdf.params(model, force, handling)
     key = key + (id(masks),)
+    omega_key = getattr(model, "omega_field", None)
+    if omega_key is not None:
+        key = key + (("omega", _upload_rates(lat, omega_key)),)
+        kp.struct.omega_cells = lat.omega_ptr
     if lat.host_changed():
         lat.upload_host()
     return lat, kp, key, masks
+
+
+def _upload_rates(lat, omega_key):
+    """Per-cell SRT rates of this rank's box interior -> HBM (sweep.py:
+    138-146: validated in (0, 2) on every sweep).  Re-uploaded only when the
+    host values changed; returns the content version (a change re-collides
+    the stored state, as the reference collides with the current rates)."""
+    box = lat.box
+    dense = np.empty((box.nz, box.ny, box.nx), dtype=np.float64)
+    for block, (ox, oy, oz) in zip(box.blocks, box.offsets):
+        ow = block.data[omega_key]
+        win = ow.field.view[..., 0] if hasattr(ow, "field") else ow.view[..., 0]
+        inner = win[1:-1, 1:-1, 1:-1]
+        if np.any(inner <= 0.0) or np.any(inner >= 2.0):
+            raise ValidationError("per-cell rates must lie in (0, 2)")
+        dense[oz:oz + inner.shape[0], oy:oy + inner.shape[1], ox:ox + inner.shape[2]] = inner
+    return lat.set_rates(dense)
 
 
 def stream_collide(pdf: PdfField, model, *, force=None, handling=None) -> None:

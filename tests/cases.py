@@ -67,6 +67,15 @@ CASES = {
                              periodic=(True, False, False), geometry=dict(kind="channel2d"),
                              model=("TRT_magic", 1.2), force=("Guo", (1e-5, 0.0, 0.0)),
                              init=("random", 7), steps=25, snapshots=(25,), layout="zyxf"),
+    # per-cell SRT rates (f1 row, lbm/sweep.py:111-146): seeded rate field,
+    # spheres + z walls, general Guo force, 2 blocks in z
+    "d3q19_srt_omegafield": dict(stencil="D3Q19", dims=(10, 8, 12), root_dims=(1, 1, 2),
+                                 periodic=(True, True, False),
+                                 geometry=dict(kind="spheres", seed=21, rmin=1.5, rmax=2.5,
+                                               frac=0.15, walls_z=True),
+                                 model=("SRT_field", 21, 0.7, 1.9),
+                                 force=("Guo", (1e-4, -3e-5, 2e-5)), init=("random", 21),
+                                 steps=12, snapshots=(1, 12), layout="zyxf"),
     # Pressure anti-bounce-back (f1 row): D2Q9 box, pressure top row
     "d2q9_pressure_box": dict(stencil="D2Q9", dims=(8, 8, 1), root_dims=(1, 1, 1),
                               periodic=(False, False, False), geometry=dict(kind="pressure_box"),
@@ -190,7 +199,16 @@ def model_of(api, spec, st):
         return api.MRT(st, rates)
     if kind == "MRT_raw":
         return api.make_raw_mrt(st, m[1], m[2])
+    if kind == "SRT_field":
+        return api.SRT(omega_field="omega")
     raise ValueError(kind)
+
+
+def rate_field(spec):
+    """Global interior per-cell SRT rates (nz, ny, nx) of an SRT_field case."""
+    _, seed, lo, hi = spec["model"]
+    nx, ny, nz = spec["dims"]
+    return np.random.default_rng(seed).uniform(lo, hi, size=(nz, ny, nx))
 
 
 def force_of(api, spec):
@@ -264,6 +282,12 @@ def run_case(api, ctx, spec, *, pdf_kwargs=None):
             lo, hi = forest.cell_box(block.id)
             sl = (slice(lo[2], hi[2]), slice(lo[1], hi[1]), slice(lo[0], hi[0]))
             pdf.src(block).interior[...] = api.equilibrium(rho[sl], u[sl], st)
+    if spec["model"][0] == "SRT_field":
+        forest.register_data("omega", api.FieldDataHandler(nf=1, ghost_layers=1))
+        om = rate_field(spec)
+        for block in forest.local_blocks():
+            lo, hi = forest.cell_box(block.id)
+            block.data["omega"].interior[..., 0] = om[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
     model = model_of(api, spec, st)
     force = force_of(api, spec)
     out = {"pdf": {}, "macro": None, "links": None}
@@ -360,6 +384,11 @@ def oracle_model(spec, oracle):
     fk = "guo" if f is None or f[0] == "Guo" else "shift"
     if m[0] == "SRT":
         return oracle.Model("SRT", omega=m[1], force=force, force_kind=fk)
+    if m[0] == "SRT_field":
+        nx, ny, nz = spec["dims"]
+        of = np.zeros((nz + 2, ny + 2, nx + 2))
+        of[1:-1, 1:-1, 1:-1] = rate_field(spec)
+        return oracle.Model("SRT", omega=0.0, omega_field=of, force=force, force_kind=fk)
     if m[0] in ("TRT", "TRT_magic"):
         we, wo = (m[1], m[2]) if m[0] == "TRT" else oracle.trt_magic(m[1])
         return oracle.Model("TRT", omega_e=we, omega_o=wo, force=force, force_kind=fk)

@@ -50,9 +50,13 @@ def run_ref(spec, n_ranks=1):
     return SimRuntime(n_ranks, seed=0).run(lambda ctx: cases.run_case(api, ctx, spec))[0]
 
 
-def main():
-    meta = {}
+def main(only=None):
+    """only: case names to (re)generate; the other entries of digests.json
+    and the unit vectors are kept as committed."""
+    meta = json.loads((HERE / "digests.json").read_text()) if only else {}
     for name, spec in cases.CASES.items():
+        if only and name not in only:
+            continue
         res = run_ref(spec)
         if spec["root_dims"][2] >= 2 or spec["root_dims"][0] >= 2:
             res2 = run_ref(spec, 2)
@@ -70,6 +74,9 @@ def main():
         np.savez(HERE / f"{name}.npz", **arrays)
         meta[name] = {"digests": digests, "links": links, "spec": repr(spec)}
         print(name, {k: v[:12] for k, v in digests.items()}, links, flush=True)
+    (HERE / "digests.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
+    if only:
+        return
     dig = {}
     for name, spec in cases.DIGEST_CASES.items():
         res = run_ref(spec)
@@ -128,4 +135,5 @@ def make_units():
 
 
 if __name__ == "__main__":
-    main()
+    # python tests/golden/make_golden.py [case ...]   (no args: everything)
+    main(sys.argv[1:] or None)

@@ -26,7 +26,7 @@ def test_library_loads_and_exports_every_header_symbol():
     assert sorted(syms) == sorted(_lib.EXPORTS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.lbm_abi_version() == 1
+    assert lib.lbm_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_is_sm100a():
@@ -178,8 +178,10 @@ def test_kernel_params_host_constants():
     assert srt.rem == 1.0 - 1.8 and srt.hw == 1.0 - 0.5 * 1.8
     with pytest.raises(P.ValidationError):
         P.kernel_params(st, P.TRT(1.2, 1.1), P.SimpleShift((1e-5, 0, 0)))
+    # per-cell rates: model LBM_SRT_FIELD, the sweep supplies the device rates
+    assert P.kernel_params(st, P.SRT(omega_field="om")).struct.model == _lib.SRT_FIELD
     with pytest.raises(P.ValidationError):
-        P.kernel_params(st, P.SRT(omega_field="om"))
+        P.kernel_params(st, P.SRT(omega_field="om"), P.SimpleShift((1e-5, 0, 0)))
 
 
 def test_mrt_tables_match_reference():

@@ -328,3 +328,63 @@ def test_rank_invariance_periodic_z_two_ranks(api):
     multi = P.run(2, _rank_prog, spec, backend="gloo", device="cuda")[0]
     assert multi["pdf"][8].tobytes() == base["pdf"][8].tobytes()
     assert base["pdf"][8].tobytes() == cases.oracle_run(spec, oracle)["pdf"][8].tobytes()
+
+
+def test_rate_field_change_between_sweeps_matches_oracle(api):
+    """Per-cell SRT rates (lbm/sweep.py:111-146) are read on every sweep:
+    editing the rate field between calls re-collides the stored state with
+    the new rates (oracle, bitwise); out-of-range rates raise."""
+    import paper_1909_13772_b200 as P
+    spec = dict(cases.CASES["d3q19_srt_omegafield"])
+    nx, ny, nz = spec["dims"]
+    ctx = _ctx()
+    forest = P.create_forest(ctx, (0, 0, 0, 1, 1, 1), (1, 1, 1), periodic=(True, True, True),
+                             cells_per_block=(nx, ny, nz))
+    pdf = P.PdfField(forest, P.D3Q19, layout="fzyx")
+    P.fill_equilibrium(pdf)
+    rho, u = cases.workloads.random_rho_u((nx, ny, nz), 5)
+    blk = forest.local_blocks()[0]
+    pdf.src(blk).interior[...] = P.equilibrium(rho, u, P.D3Q19)
+    forest.register_data("omega", P.FieldDataHandler(nf=1, ghost_layers=1))
+    om1 = cases.rate_field(spec)
+    om2 = np.random.default_rng(99).uniform(0.6, 1.95, size=om1.shape)
+    force = P.Guo((2e-5, 0.0, -1e-5))
+    blk.data["omega"].interior[..., 0] = om1
+    for _ in range(4):
+        P.stream_collide(pdf, P.SRT(omega_field="omega"), force=force)
+    blk.data["omega"].interior[..., 0] = om2
+    for _ in range(3):
+        P.stream_collide(pdf, P.SRT(omega_field="omega"), force=force)
+    got = pdf.src(blk).interior.copy()
+    st = oracle.STENCILS["D3Q19"]
+    full = np.zeros((st.q, nz + 2, ny + 2, nx + 2))
+    full[:, 1:-1, 1:-1, 1:-1] = np.moveaxis(oracle.equilibrium(rho, u, st), 3, 0)
+    feq0 = oracle.equilibrium(np.ones((nz + 2, ny + 2, nx + 2)), np.zeros((nz + 2, ny + 2, nx + 2, 3)), st)
+    ghost = np.ones((nz + 2, ny + 2, nx + 2), bool)
+    ghost[1:-1, 1:-1, 1:-1] = False
+    full[:, ghost] = np.moveaxis(feq0, 3, 0)[:, ghost]
+    doms = []
+    for om in (om1, om2):
+        of = np.zeros((nz + 2, ny + 2, nx + 2))
+        of[1:-1, 1:-1, 1:-1] = om
+        doms.append(oracle.Domain(st, (nx, ny, nz), (True, True, True),
+                                  oracle.Model("SRT", omega=0.0, omega_field=of,
+                                               force=(2e-5, 0.0, -1e-5))))
+    doms[0].set_full(full)
+    doms[0].run(4)
+    doms[1].set_full(doms[0].a)
+    doms[1].run(3)
+    assert got.tobytes() == doms[1].rform().tobytes()
+    blk.data["omega"].interior[0, 0, 0, 0] = 2.0
+    with pytest.raises(P.ValidationError):
+        P.stream_collide(pdf, P.SRT(omega_field="omega"))
+
+
+def test_rate_field_fp32_within_tolerance(api):
+    spec = dict(cases.CASES["d3q19_srt_omegafield"])
+    spec.update(steps=100, snapshots=(100,))
+    res = cases.run_case(api, _ctx(), spec, pdf_kwargs={"dtype": "float32"})
+    ores = cases.oracle_run(spec, oracle)
+    a, b = res["pdf"][100], ores["pdf"][100]
+    rel = float(np.max(np.abs(a - b) / np.abs(b)))
+    assert rel < TOL_F32_REL, rel
