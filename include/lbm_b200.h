@@ -36,9 +36,9 @@
  *                       PDF directions that cross the face.
  *
  * Device PDF layout ("z-q-y-x", one box per rank, one ghost layer on every
- * side):  element (z, slot, y, x) lives at
+ * side):  direction i of cell (z, y, x) lives at
  *     ((z+1) * q + slot) * plane + (y+1) * pitch + xoff + x
- * with plane = (ny+2) * pitch.  Direction i is stored in slot
+ * with plane = (ny+2) * pitch and slot = lbm_slot_of(q, i).  Direction i is stored in slot
  * lbm_slot_of(q, i): slots are grouped by c_z (-1, 0, +1), so the directions
  * that cross a z-face form ONE contiguous run per z-plane and the halo can be
  * sent straight out of / into the field (zero-copy NCCL send/recv).
