@@ -261,6 +261,11 @@ def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # torchrun pins OMP_NUM_THREADS=1 per process; the reference arm runs on
+    # rank 0 alone and uses every host thread (set before libgomp loads)
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle
+    os.environ["OMP_NUM_THREADS"] = str(oracle.threads_available())
     base = cpu_reference(cfg, args.steps, args.warmup, max(args.cpu_seconds, 60.0))
     line = {"impl": "reference", "metric": "MLUPS", "value": base["value"], "unit": "MLUPS",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,

@@ -31,8 +31,8 @@ class Context:
             self.rank, self.n_ranks, self.backend = 0, 1, None
         if device is None:
             if torch.cuda.is_available():
-                local = int(os.environ.get("LOCAL_RANK", self.rank % max(1, torch.cuda.device_count())))
-                device = torch.device("cuda", local)
+                local = int(os.environ.get("LOCAL_RANK", self.rank))
+                device = torch.device("cuda", local % max(1, torch.cuda.device_count()))
             else:
                 device = torch.device("cpu")
         self.device = torch.device(device)
@@ -81,13 +81,19 @@ def init_distributed(backend: str | None = None) -> Context:
     """Initialise torch.distributed from the torchrun environment (RANK,
     WORLD_SIZE, MASTER_ADDR, MASTER_PORT) and return the rank context."""
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1 and not dist.is_initialized():
+        # LBM_B200_BACKEND=gloo: several ranks sharing one GPU (host-staged
+        # halos; the multi-rank bench smoke on a single-GPU box)
+        backend = backend or os.environ.get("LBM_B200_BACKEND")
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         import datetime
+        kw = {}
+        if backend == "nccl":
+            dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+            torch.cuda.set_device(dev)
+            kw["device_id"] = dev     # eager communicator init, device-bound barriers
         # fail instead of hanging forever if a peer dies mid-exchange
-        dist.init_process_group(backend=backend, timeout=datetime.timedelta(seconds=600))
+        dist.init_process_group(backend=backend, timeout=datetime.timedelta(seconds=600), **kw)
     return Context()
 
 
