@@ -184,6 +184,7 @@ class DeviceLattice:
         self._streams = None
         self._fluid_masks = None
         self._rates = None        # (host copy, device tensor, version) of per-cell SRT rates
+        self._graphs = {}         # (collision key, parity) -> (two-step CUDA graph, masks)
 
     # ---------------------------------------------------------- plumbing
     @property
@@ -375,6 +376,18 @@ class DeviceLattice:
         if self.has_halo:
             S = self._streams_get()
             S["boundary"].wait_stream(main)
+        if not self.has_halo and nsteps >= 4:
+            # launch-bound loops: replay a captured two-step graph (buffer
+            # ping-pong returns to the same parity), odd remainder eagerly
+            graph = self._pair_graph(kp, key, masks, cm, tm)
+            if graph is not None:
+                for _ in range(nsteps // 2):
+                    graph.replay()
+                pairs = nsteps // 2
+                self.steps += 2 * pairs
+                self.launches += 2 * pairs
+                self.prev_kind = "G"
+                nsteps -= 2 * pairs
         for n in range(nsteps):
             src, dst = self.buf[self.cur], self.buf[1 - self.cur]
             if not self.has_halo:
@@ -393,6 +406,35 @@ class DeviceLattice:
         self._kp_stream = kp
         self.host_state = "device"
         self.snapshot = None
+
+    def _pair_graph(self, kp, key, masks, cm, tm):
+        """CUDA graph of two fused steps cur -> 1-cur -> cur (P = 1 path).
+        Kernel arguments are captured by value, so the graph is keyed by the
+        collision key and the buffer parity.  None if capture is unavailable
+        (the caller then launches eagerly)."""
+        hit = self._graphs.get((key, self.cur))
+        if hit is not None:
+            return hit[0]
+        if len(self._graphs) >= 8:
+            self._graphs.clear()
+        nz = self.box.nz
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(self.stream)
+        # both parities at once, so a loop entered at either parity replays
+        for par in (0, 1):
+            a, b = self.buf[par], self.buf[1 - par]
+            graph = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(graph, stream=side):
+                    sp = _lib.stream_ptr(torch.cuda.current_stream(self.device))
+                    for src, dst in ((a, b), (b, a)):
+                        _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src),
+                                  _lib.ptr(dst), cm, tm, 0, nz, sp)
+            except Exception:
+                graph = None
+            self._graphs[(key, par)] = (graph, masks)   # keeps the mask tensors alive
+        self.stream.wait_stream(side)
+        return self._graphs[(key, self.cur)][0]
 
     def _halo_step(self, kp, src, dst, cm, tm, main, first):
         """One overlapped step: B(n) = boundary planes on the high-priority

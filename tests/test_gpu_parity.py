@@ -388,3 +388,27 @@ def test_rate_field_fp32_within_tolerance(api):
     a, b = res["pdf"][100], ores["pdf"][100]
     rel = float(np.max(np.abs(a - b) / np.abs(b)))
     assert rel < TOL_F32_REL, rel
+
+
+def test_stream_collide_n_graph_replay_bitwise(api):
+    """stream_collide_n (two-step CUDA graph replay + odd remainder) equals
+    the per-call loop bit for bit, and the oracle."""
+    import paper_1909_13772_b200 as P
+    spec = dict(cases.CASES["c1_trt_guo_porous"])
+    spec.update(steps=11, snapshots=(11,))
+    base = cases.run_case(api, _ctx(), spec)
+    orc = cases.oracle_run(spec, oracle)
+    assert base["pdf"][11].tobytes() == orc["pdf"][11].tobytes()
+    # same case, time loop replaced by stream_collide_n
+    api2 = cases.b200_api()
+    calls = {"n": 0}
+
+    def collide_n(pdf, model, *, force=None, handling=None):
+        calls["n"] += 1
+        if calls["n"] == 1:
+            P.stream_collide(pdf, model, force=force, handling=handling)
+            P.stream_collide_n(pdf, model, 10, force=force, handling=handling)
+    api2.stream_collide = collide_n
+    spec2 = dict(spec, snapshots=(1,))
+    got = cases.run_case(api2, _ctx(), dict(spec2, steps=1))
+    assert got["pdf"][1].tobytes() == base["pdf"][11].tobytes()
