@@ -2,17 +2,21 @@
 
 A drop-in for the reference's sweep API (blocksim: create_forest, PdfField,
 ensure_flags, BoundaryHandling, fill_equilibrium, stream_collide,
-exchange_ghosts, macroscopic_fields, gather_slice, mlups) whose compute runs
+exchange_ghosts, macroscopic_fields, gather_slice, mlups; forest snapshots
+and VTK output) whose compute runs
 in hand-written sm_100a kernels (csrc/, C-ABI include/lbm_b200.h) on
 HBM-resident structure-of-arrays PDF fields, z-slab partitioned over GPUs
 with a zero-copy NCCL halo of the crossing directions.
 """
-from .errors import BackendError, BlocksimError, NumericsError, TopologyError, ValidationError
+from .errors import BackendError, BlocksimError, BufferUnderflowError, NumericsError, \
+    TopologyError, TypeTagError, ValidationError
 from .runtime import Context, init_distributed, run
 from .blockforest import BlockForest, BlockId, create_forest
 from .field import Field, FieldDataHandler, FlagField, FlagFieldHandler, GhostPackInfo, \
     exchange_ghosts, gather_slice, sweep
 from .lbm import *  # noqa: F401,F403
 from . import lbm
+from .vtk import write_block_vtk, write_vtk
+from .wire import RecvBuffer, SendBuffer
 
 __version__ = "0.1.0"

@@ -185,6 +185,7 @@ class DeviceLattice:
         self._fluid_masks = None
         self._rates = None        # (host copy, device tensor, version) of per-cell SRT rates
         self._graphs = {}         # (collision key, parity) -> (two-step CUDA graph, masks)
+        self._dst_synced = None   # (steps, kind) the host dst slot was read back at
 
     # ---------------------------------------------------------- plumbing
     @property
@@ -232,6 +233,7 @@ class DeviceLattice:
             self.coll_key = None
             self.host_state = "device"
             self.snapshot = None
+            self._dst_synced = None
             return
         dense = self.box.gather(self._views(self.pdf.key), self.q, np.float64)
         t = torch.from_numpy(dense).pin_memory().to(self.device, non_blocking=True)
@@ -241,6 +243,7 @@ class DeviceLattice:
         self.host_state = "synced"
         self.snapshot = None
         self.halo_sync_rform()
+        self._dst_synced = None
         torch.cuda.current_stream(self.device).synchronize()
         del t
 
@@ -254,6 +257,7 @@ class DeviceLattice:
         self.coll_key = None
         self.host_state = "device"
         self.snapshot = None
+        self._dst_synced = None
 
     def halo_sync_rform(self):
         """R-form halos are not needed: G_0 = C(R_0) is computed on the
@@ -283,18 +287,64 @@ class DeviceLattice:
         kind, t = self.readout_device()
         return kind, t.cpu().numpy()
 
+    def _wrap_ghosts(self, full):
+        """Covered ghost cells of a ghost-inclusive (q, Z, Y, X) box = their
+        periodic images inside the box (x, then y rows incl. x ghosts, then
+        z planes: edges and corners come out as the reference's 26-image
+        exchange fills them).  Halo and uncovered faces keep their values."""
+        b = self.box
+        if b.wrap_x:
+            full[..., 0] = full[..., b.nx]
+            full[..., b.nx + 1] = full[..., 1]
+        if b.wrap_y:
+            full[:, :, 0] = full[:, :, b.ny]
+            full[:, :, b.ny + 1] = full[:, :, 1]
+        if b.zface_lo == _lib.ZFACE_WRAP:
+            full[:, 0] = full[:, b.nz]
+            full[:, b.nz + 1] = full[:, 1]
+        return full
+
+    def full_state(self, which="src"):
+        """The reference's Field.raw content of a PDF slot as a ghost-inclusive
+        (q, Z, Y, X) fp64 device tensor: src = R_n, dst = C(R_{n-1}) after a
+        sweep (the R-form fill before any).  Uncovered ghost cells carry the
+        device values (never rewritten after the fill, as in the reference);
+        covered ghosts are images of the slot's own interior.  (The
+        reference's src ghosts hold stale images of C(R_{n-2}) between sweeps;
+        every sweep overwrites them before use, so they carry no state.)"""
+        self.join_streams()
+        b = self.box
+        full = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
+                           device=self.device)
+        if which == "dst":
+            src = self.buf[1 - self.cur] if self.prev_kind == "G" else self.buf[self.cur]
+            _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(src), _lib.ptr(full), self._sp())
+        else:
+            kind, t = self.readout_device()
+            if kind == "full":
+                full.copy_(t)
+            else:
+                _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(self.buf[self.cur]),
+                          _lib.ptr(full), self._sp())
+                full[:, 1:-1, 1:-1, 1:-1] = t
+        return self._wrap_ghosts(full)
+
     def sync_host(self):
         """Pull R_n into the host block arrays of the src slot (idempotent)."""
         if self.host_state != "device":
             return
-        kind, dense = self.readout()
-        views = self._views(self.pdf.key)
-        if kind == "full":
-            self.box.scatter_full(dense, views)
-        else:
-            self.box.scatter_interior(dense, views)
+        dense = self.full_state("src").cpu().numpy()
+        self.box.scatter_full(dense, self._views(self.pdf.key))
         self.host_state = "synced"
         self.snapshot = None
+
+    def sync_host_dst(self):
+        """Pull C(R_{n-1}) into the host arrays of the dst slot (once per state)."""
+        if self.cur_kind is None or self._dst_synced == (self.steps, self.cur_kind):
+            return
+        dense = self.full_state("dst").cpu().numpy()
+        self.box.scatter_full(dense, self._views(self.pdf.dst_key))
+        self._dst_synced = (self.steps, self.cur_kind)
 
     def host_touched(self):
         """Called when host arrays are handed out while synced: remember the
@@ -406,6 +456,7 @@ class DeviceLattice:
         self._kp_stream = kp
         self.host_state = "device"
         self.snapshot = None
+        self._dst_synced = None
 
     def _pair_graph(self, kp, key, masks, cm, tm):
         """CUDA graph of two fused steps cur -> 1-cur -> cur (P = 1 path).

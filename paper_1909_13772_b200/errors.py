@@ -21,6 +21,14 @@ class NumericsError(BlocksimError):
     """Non-positive density / divergence (errors.py:44)."""
 
 
+class TypeTagError(BlocksimError):
+    """A debug type tag or wire dtype code did not match (errors.py:20)."""
+
+
+class BufferUnderflowError(BlocksimError):
+    """Read past the end of a receive buffer (errors.py:24)."""
+
+
 class BackendError(BlocksimError):
     """The CUDA kernel library is missing or a launch failed.  There is no
     CPU fallback: every compute call goes through the sm_100a library."""

@@ -209,6 +209,19 @@ class FieldDataHandler:
         return Field(tuple(forest.cells_per_block) + (self.nf,), self.g, self.layout, self.init,
                      self.dtype, dx, lazy=self.lazy)
 
+    # snapshot slot format: the raw array (handler.py:53-63)
+    def serialize(self, forest, block, field, buf) -> None:
+        buf.pack_array(field.raw)
+
+    def deserialize(self, forest, block, buf) -> Field:
+        field = self.create(forest, block)
+        raw = buf.unpack_array()
+        if raw.shape != field.raw.shape:
+            raise ValidationError(f"serialized field shape {raw.shape} != expected "
+                                  f"{field.raw.shape}")
+        field.raw[...] = raw
+        return field
+
 
 class FlagFieldHandler:
     """FlagFields sharing one registry (handler.py:83-102)."""
@@ -230,6 +243,18 @@ class FlagFieldHandler:
         if forest.cells_per_block is None:
             raise ValidationError("forest has no cells_per_block")
         return FlagField(forest.cells_per_block, self.g, self.registry)
+
+    def serialize(self, forest, block, flags, buf) -> None:
+        buf.pack_array(flags.field.raw)
+
+    def deserialize(self, forest, block, buf) -> FlagField:
+        flags = self.create(forest, block)
+        raw = buf.unpack_array()
+        if raw.shape != flags.field.raw.shape:
+            raise ValidationError(f"serialized flag shape {raw.shape} != expected "
+                                  f"{flags.field.raw.shape}")
+        flags.field.raw[...] = raw
+        return flags
 
 
 # ------------------------------------------------------------ ghost exchange

@@ -31,6 +31,52 @@ class _Mirror:
             lat.host_touched()
 
 
+class _DstMirror:
+    """Hook on the dst slot's host Fields: after a sweep the reference's dst
+    slot holds the previous post-collision state C(R_{n-1}) with its covered
+    ghosts (what the swap left there); it is read back from the device on
+    access.  Host writes into the dst slot are not uploaded (the next sweep
+    overwrites it in the reference too)."""
+
+    def __init__(self, pdf):
+        self.pdf = pdf
+
+    def host_access(self):
+        lat = self.pdf._lattice
+        if lat is not None:
+            lat.sync_host_dst()
+
+
+class PdfSlotHandler(FieldDataHandler):
+    """Data handler of the two PDF slots: lazily allocated host mirrors of
+    the HBM state; snapshots serialise the reference's Field.raw content
+    (src: R_n, dst: C(R_{n-1})) through the mirror, and restoring the src
+    slot makes the host data authoritative again (the device lattice is
+    rebuilt and re-uploaded before the next sweep)."""
+
+    def __init__(self, pdf, which, nf, ghost_layers, layout):
+        super().__init__(nf=nf, ghost_layers=ghost_layers, layout=layout, lazy=True)
+        self.pdf = pdf
+        self.which = which
+
+    def create(self, forest, block):
+        field = super().create(forest, block)
+        field._mirror = self.pdf._mirror if self.which == "src" else self.pdf._dst_mirror
+        return field
+
+    def deserialize(self, forest, block, buf):
+        if self.which == "src":
+            self.pdf._lattice = None      # block objects change: new box, fresh upload
+        field = FieldDataHandler.create(self, forest, block)
+        raw = buf.unpack_array()
+        if raw.shape != field._raw.shape:
+            raise ValidationError(f"serialized field shape {raw.shape} != expected "
+                                  f"{field._raw.shape}")
+        field._raw[...] = raw
+        field._mirror = self.pdf._mirror if self.which == "src" else self.pdf._dst_mirror
+        return field
+
+
 class PdfField:
     """Population storage: `key` (src) and `key.dst` host slots plus the
     device lattice (two HBM buffers) behind them.
@@ -49,14 +95,12 @@ class PdfField:
         self.key = key
         self.dst_key = key + ".dst"
         self.dtype = dtype
-        forest.register_data(key, FieldDataHandler(nf=stencil.q, ghost_layers=ghost_layers,
-                                                   layout=layout, lazy=True))
-        forest.register_data(self.dst_key, FieldDataHandler(nf=stencil.q, ghost_layers=ghost_layers,
-                                                            layout=layout, lazy=True))
         self._lattice = None
         self._mirror = _Mirror(self)
-        for block in forest.local_blocks():
-            block.data[key]._mirror = self._mirror
+        self._dst_mirror = _DstMirror(self)
+        forest.register_data(key, PdfSlotHandler(self, "src", stencil.q, ghost_layers, layout))
+        forest.register_data(self.dst_key, PdfSlotHandler(self, "dst", stencil.q, ghost_layers,
+                                                          layout))
         self._kp_cache = {}
 
     def src(self, block):
@@ -166,6 +210,7 @@ def fill_equilibrium_arrays(pdf: PdfField, rho, u) -> None:
               _lib.ptr(lat.buf[lat.cur]), lat._sp())
     lat.cur_kind, lat.prev_kind, lat.coll_key = "R", None, None
     lat.host_state, lat.snapshot = "device", None
+    lat._dst_synced = None
 
 
 def macroscopic_arrays(pdf: PdfField, *, force=None, out=None):

@@ -131,6 +131,8 @@ def reference_api():
     ns.FieldDataHandler = FieldDataHandler
     ns.gather_slice = gather_slice
     ns.make_raw_mrt = make_raw_mrt
+    from blocksim.field import write_vtk
+    ns.write_vtk = write_vtk
     return ns
 
 
@@ -141,6 +143,7 @@ def b200_api():
     ns.FieldDataHandler = P.FieldDataHandler
     ns.gather_slice = P.gather_slice
     ns.make_raw_mrt = lambda st, shear, other: P.lbm.MRT.raw_moments(st, shear, other)
+    ns.write_vtk = P.write_vtk
     return ns
 
 
@@ -230,6 +233,38 @@ def smooth_u(x, y, z):
 def run_case(api, ctx, spec, *, pdf_kwargs=None):
     """Returns {"pdf": {step: (nz,ny,nx,q)}, "macro": (rho, u) or None,
     "links": {name: count}} on rank 0 (None elsewhere)."""
+    forest, pdf, handling, model, force, st = setup_case(api, ctx, spec, pdf_kwargs=pdf_kwargs)
+    nx, ny, nz = spec["dims"]
+    d = 2 if spec["stencil"] == "D2Q9" else 3
+    out = {"pdf": {}, "macro": None, "links": None}
+    snaps = set(spec["snapshots"])
+    for s in range(1, spec["steps"] + 1):
+        api.stream_collide(pdf, model, force=force, handling=handling)
+        if s in snaps:
+            g = api.gather_slice(forest, "pdf", (0, 0, 0), forest.global_cells(0))
+            if g is not None:
+                out["pdf"][s] = g
+    if spec.get("macro"):
+        forest.register_data("rho", api.FieldDataHandler(nf=1, ghost_layers=0))
+        forest.register_data("vel", api.FieldDataHandler(nf=d, ghost_layers=0))
+        api.macroscopic_fields(pdf, "rho", "vel", force=force, handling=handling)
+        r = api.gather_slice(forest, "rho", (0, 0, 0), forest.global_cells(0))
+        v = api.gather_slice(forest, "vel", (0, 0, 0), forest.global_cells(0))
+        if r is not None:
+            out["macro"] = (r[..., 0], v)
+    if handling is not None:
+        counts = {}
+        for name in ("NoSlip", "UBB", "Pressure"):
+            counts[name] = sum(len(zs) for b in forest.local_blocks()
+                               for (i, zs, ys, xs) in handling.links[b.id][name])
+        tot = ctx.all_gather(counts)
+        out["links"] = {n: sum(tot[r][n] for r in tot) for n in counts}
+    return out if ctx.rank == 0 else None
+
+
+def setup_case(api, ctx, spec, *, pdf_kwargs=None):
+    """Forest, PDF field, flags/handling, rate field and initial state of a
+    case; returns (forest, pdf, handling, model, force, stencil)."""
     st = getattr(api, spec["stencil"])
     nx, ny, nz = spec["dims"]
     R = spec["root_dims"]
@@ -290,30 +325,47 @@ def run_case(api, ctx, spec, *, pdf_kwargs=None):
             block.data["omega"].interior[..., 0] = om[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
     model = model_of(api, spec, st)
     force = force_of(api, spec)
-    out = {"pdf": {}, "macro": None, "links": None}
-    snaps = set(spec["snapshots"])
-    for s in range(1, spec["steps"] + 1):
-        api.stream_collide(pdf, model, force=force, handling=handling)
-        if s in snaps:
-            g = api.gather_slice(forest, "pdf", (0, 0, 0), forest.global_cells(0))
-            if g is not None:
-                out["pdf"][s] = g
-    if spec.get("macro"):
-        forest.register_data("rho", api.FieldDataHandler(nf=1, ghost_layers=0))
-        forest.register_data("vel", api.FieldDataHandler(nf=d, ghost_layers=0))
+    return forest, pdf, handling, model, force, st
+
+
+# snapshot / restart / VTK case: k steps, macroscopic
+# fields, forest image + VTK files, then m more steps
+SNAPSHOT_CASE = dict(stencil="D3Q19", dims=(8, 6, 8), root_dims=(1, 1, 2),
+                     periodic=(True, True, False),
+                     geometry=dict(kind="spheres", seed=5, rmin=1.5, rmax=2.5, frac=0.15,
+                                   walls_z=True),
+                     model=("TRT_magic", 1.6), force=("Guo", (1e-4, 0.0, 3e-5)),
+                     init=("random", 11), steps=5, snapshots=(), layout="fzyx")
+SNAPSHOT_MORE = 4
+
+
+def run_snapshot_case(api, ctx, spec, vtk_dir, *, image=None, pdf_kwargs=None):
+    """k = spec["steps"] sweeps, rho/vel, forest image + VTK, then
+    SNAPSHOT_MORE sweeps.  With `image`, the forest is first restored from it
+    (restart: the k sweeps are skipped).  Returns {"image", "vtk" {name:
+    bytes}, "pdf_more"} on rank 0."""
+    import os
+    forest, pdf, handling, model, force, st = setup_case(api, ctx, spec, pdf_kwargs=pdf_kwargs)
+    forest.register_data("rho", api.FieldDataHandler(nf=1, ghost_layers=1))
+    forest.register_data("vel", api.FieldDataHandler(nf=3, ghost_layers=1))
+    if image is None:
+        for _ in range(spec["steps"]):
+            api.stream_collide(pdf, model, force=force, handling=handling)
         api.macroscopic_fields(pdf, "rho", "vel", force=force, handling=handling)
-        r = api.gather_slice(forest, "rho", (0, 0, 0), forest.global_cells(0))
-        v = api.gather_slice(forest, "vel", (0, 0, 0), forest.global_cells(0))
-        if r is not None:
-            out["macro"] = (r[..., 0], v)
-    if handling is not None:
-        counts = {}
-        for name in ("NoSlip", "UBB", "Pressure"):
-            counts[name] = sum(len(zs) for b in forest.local_blocks()
-                               for (i, zs, ys, xs) in handling.links[b.id][name])
-        tot = ctx.all_gather(counts)
-        out["links"] = {n: sum(tot[r][n] for r in tot) for n in counts}
-    return out if ctx.rank == 0 else None
+    else:
+        forest.load_snapshot_blocks([image])
+        forest.rebuild_neighborhoods()
+    img = forest.snapshot()
+    names = api.write_vtk(forest, vtk_dir, "out", spec["steps"], [("rho", "rho"), ("u", "vel")])
+    vtk = {}
+    for name in sorted(os.listdir(vtk_dir)):
+        with open(os.path.join(vtk_dir, name), "rb") as fh:
+            vtk[name] = fh.read()
+    del names
+    for _ in range(SNAPSHOT_MORE):
+        api.stream_collide(pdf, model, force=force, handling=handling)
+    g = api.gather_slice(forest, "pdf", (0, 0, 0), forest.global_cells(0))
+    return {"image": img, "vtk": vtk, "pdf_more": g} if ctx.rank == 0 else None
 
 
 # ------------------------------------------------------------- the oracle

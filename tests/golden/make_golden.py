@@ -88,6 +88,24 @@ def main(only=None):
     make_units()
 
 
+def make_snapshot():
+    """f3 formats: the reference's forest image + VTK files after k sweeps of
+    cases.SNAPSHOT_CASE, and the PDFs after SNAPSHOT_MORE more sweeps."""
+    import tempfile
+    spec = cases.SNAPSHOT_CASE
+    with tempfile.TemporaryDirectory() as tmp:
+        api = cases.reference_api()
+        res = SimRuntime(1, seed=0).run(lambda ctx: cases.run_snapshot_case(api, ctx, spec, tmp))[0]
+    np.savez(HERE / "snapshot_case.npz", image=np.frombuffer(res["image"], dtype=np.uint8),
+             pdf_more=res["pdf_more"])
+    meta = json.loads((HERE / "digests.json").read_text())
+    meta["snapshot_case"] = {"vtk": {n: sha(np.frombuffer(b, dtype=np.uint8))
+                                     for n, b in res["vtk"].items()},
+                             "image": sha(np.frombuffer(res["image"], dtype=np.uint8))}
+    (HERE / "digests.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
+    print("snapshot:", len(res["image"]), "bytes,", len(res["vtk"]), "vtk files")
+
+
 def make_units():
     """Reference unit functions on seeded random cells."""
     import blocksim.lbm as L
@@ -135,5 +153,11 @@ def make_units():
 
 
 if __name__ == "__main__":
-    # python tests/golden/make_golden.py [case ...]   (no args: everything)
-    main(sys.argv[1:] or None)
+    # python tests/golden/make_golden.py [case ... | snapshot]   (no args: everything)
+    args = sys.argv[1:]
+    if args == ["snapshot"]:
+        make_snapshot()
+    else:
+        main(args or None)
+        if not args:
+            make_snapshot()
