@@ -251,8 +251,8 @@ def equilibrium(rho, velocity, stencil: Stencil):
     if u.shape[-1] != 3:
         raise ValidationError(f"velocity needs 2 or 3 components, got shape {u.shape}")
     shape = np.broadcast(rho, u[..., 0]).shape
-    r = np.ascontiguousarray(np.broadcast_to(rho, shape)).reshape(-1)
-    uu = np.ascontiguousarray(np.broadcast_to(u, shape + (3,))).reshape(-1, 3)
+    r = np.array(np.broadcast_to(rho, shape), dtype=np.float64).reshape(-1)
+    uu = np.array(np.broadcast_to(u, shape + (3,)), dtype=np.float64).reshape(-1, 3)
     n = r.size
     dev = _device()
     tr = torch.from_numpy(r).to(dev)

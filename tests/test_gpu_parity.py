@@ -412,3 +412,17 @@ def test_stream_collide_n_graph_replay_bitwise(api):
     spec2 = dict(spec, snapshots=(1,))
     got = cases.run_case(api2, _ctx(), dict(spec2, steps=1))
     assert got["pdf"][1].tobytes() == base["pdf"][11].tobytes()
+
+
+@pytest.mark.parametrize("name", sorted(cases.CASES))
+def test_fp32_every_golden_case_within_1e5_relative(api, name):
+    """fp32 storage with fp32 centred arithmetic on every golden case (all
+    stencils, models, forces and boundary types) against the reference's fp64
+    golden vectors at BASELINE's 1e-5 relative tolerance."""
+    spec = cases.CASES[name]
+    res = cases.run_case(api, _ctx(), spec, pdf_kwargs={"dtype": "float32"})
+    gold = np.load(GOLDEN / f"{name}.npz")
+    for s, arr in res["pdf"].items():
+        ref = gold[f"pdf_{s}"]
+        rel = float(np.max(np.abs(arr - ref) / np.abs(ref)))
+        assert rel < TOL_F32_REL, (name, s, rel)
