@@ -31,6 +31,10 @@
  *   lbm_collide_cells / lbm_equilibrium_cells / lbm_macroscopic_cells
  *                       collide_pdfs / equilibrium / macroscopic on flat
  *                       (n, q) populations (lbm/collision.py:138-184,245-261).
+ *   lbm_build_moving_masks  map_bodies' link enumeration on the device
+ *                       (coupling/mapping.py:133-150) for moving_boundary_sweep
+ *                       (coupling/sweep.py:45-155; the wall rule itself is
+ *                       fused into lbm_fused_step through lbm_params_t.moving).
  *   lbm_face_span       geometry of the per-step z-face ghost exchange
  *                       (field/ghost.py:112-173,202-264), restricted to the
  *                       PDF directions that cross the face.
@@ -55,7 +59,7 @@
 extern "C" {
 #endif
 
-#define LBM_B200_ABI_VERSION 2
+#define LBM_B200_ABI_VERSION 3
 
 /* status codes */
 #define LBM_OK 0
@@ -87,6 +91,7 @@ extern "C" {
 #define LBM_MASK_FLUID 0x1u        /* bit 0: cell is collided              */
 #define LBM_MASK_UBB 0x80000000u   /* bit 31: some link of the cell is UBB */
 #define LBM_MASK_PRESSURE 0x40000000u /* bit 30: some link is Pressure      */
+#define LBM_MASK_MOVING 0x20000000u   /* bit 29: some link is a moving-body wall */
 /* bits 1..q-1: pulled direction i comes from a boundary cell, i.e. the
  * reference link (x, opp(i)) exists (boundary.py:91-95). */
 
@@ -101,6 +106,28 @@ typedef struct lbm_grid {
     int zface_lo;   /* LBM_ZFACE_* for the z = -1 side              */
     int zface_hi;   /* LBM_ZFACE_* for the z = nz side              */
 } lbm_grid_t;
+
+/* Moving-body walls of one sweep (coupling/sweep.py:45-155): links from
+ * fluid cells to body-covered cells bounce back with the body's surface
+ * velocity at the link midpoint, R[x, opp(i)] = G[x, i] - ((6 w_i) rho0)
+ * (c_i . u_w), u_w = v + omega x r, and hand the momentum
+ * (2 G[x, i] - ((6 w_i) rho0)(c_i . u_w)) c_i (and its torque) to the body.
+ * All pointers are DEVICE pointers; arrays cover this rank's box. */
+typedef struct lbm_moving {
+    const int32_t* owner;      /* (nz+2, ny+2, nx+2) ghost-inclusive: body slot covering the
+                                  cell, -1 where free                                       */
+    const uint32_t* linkmask;  /* (nz, ny, nx): pulled directions j whose source x - c_j is
+                                  covered (from lbm_build_moving_masks)                     */
+    const double* bodies;      /* (n_blocks * n_slots, 9): position, linear velocity, angular
+                                  velocity of the body copy each block holds (block-major)   */
+    const double* cell0;       /* (n_blocks, 3): centre of each block's first interior cell */
+    double* forces;            /* (n_blocks * n_slots, 6): force, torque accumulators (added
+                                  to; NULL = do not accumulate)                             */
+    int n_slots;               /* body slots                                                */
+    int blocks[3];             /* block grid of the box (x, y, z)                           */
+    int block_cells[3];        /* cells per block (x, y, z)                                 */
+    double rho0;               /* reference density                                         */
+} lbm_moving_t;
 
 typedef struct lbm_params {
     int model;       /* LBM_SRT / LBM_TRT / LBM_MRT                    */
@@ -126,12 +153,15 @@ typedef struct lbm_params {
      * interior, (nz, ny, nx) fp64, same cell order as the cell mask.  NULL
      * otherwise.  (ABI 2) */
     const double* omega_cells;
+    /* moving-body walls for this sweep, or NULL (ABI 3) */
+    const lbm_moving_t* moving;
 } lbm_params_t;
 
 /* ------------------------------------------------------------- metadata */
 int lbm_abi_version(void);
-/* sizeof(lbm_grid_t) (which = 0) / sizeof(lbm_params_t) (which = 1), so a
- * binding can verify its struct mirror; 0 for other values */
+/* sizeof(lbm_grid_t) (which = 0) / sizeof(lbm_params_t) (which = 1) /
+ * sizeof(lbm_moving_t) (which = 2), so a binding can verify its struct
+ * mirror; 0 for other values */
 size_t lbm_struct_size(int which);
 const char* lbm_last_error(void);
 /* storage slot of reference direction i (layout above); -1 on bad input */
@@ -201,6 +231,16 @@ int lbm_fill_equilibrium(const lbm_grid_t* g, const double* rho,
 int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags,
                        const uint32_t bits[5], uint32_t* cellmask,
                        uint32_t* typemask, int* err, void* stream);
+
+/* Combined masks of a moving-body sweep: cellmask_out = cellmask_in with
+ * LBM_MASK_FLUID cleared on covered cells (owner >= 0; they skip the
+ * collision, coupling/sweep.py:107-110) and, on the remaining fluid cells,
+ * link bit j + LBM_MASK_MOVING + linkmask bit j for every pulled direction j
+ * whose (ghost-inclusive) source cell is covered (coupling/mapping.py:
+ * 133-150).  n_links: device int, incremented by the number of links. */
+int lbm_build_moving_masks(const lbm_grid_t* g, const uint32_t* cellmask_in,
+                           const int32_t* owner, uint32_t* cellmask_out,
+                           uint32_t* linkmask, int* n_links, void* stream);
 
 /* ----------------------------------------- flat-cell utilities (n, q) */
 int lbm_collide_cells(int q, const lbm_params_t* p, double* f, int64_t n,

@@ -9,7 +9,7 @@ HBM-resident structure-of-arrays PDF fields, z-slab partitioned over GPUs
 with a zero-copy NCCL halo of the crossing directions.
 """
 from .errors import BackendError, BlocksimError, BufferUnderflowError, NumericsError, \
-    TopologyError, TypeTagError, ValidationError
+    SyncError, TopologyError, TypeTagError, ValidationError
 from .runtime import Context, init_distributed, run
 from .blockforest import BlockForest, BlockId, create_forest
 from .field import Field, FieldDataHandler, FlagField, FlagFieldHandler, GhostPackInfo, \
@@ -18,5 +18,9 @@ from .lbm import *  # noqa: F401,F403
 from . import lbm
 from .vtk import write_block_vtk, write_vtk
 from .wire import RecvBuffer, SendBuffer
+from .bodies import BodyStorage, BodyStorageHandler, RigidBody, Sphere, add_sphere, find_body, \
+    ghost_bodies, local_bodies, register_bodies, sync_bodies
+from .coupling import CoupledSystem, ParticleMapping, coupled_time_step, covered_cell_counts, \
+    map_bodies, moving_boundary_sweep, reduce_hydrodynamic_forces, reinitialize_uncovered
 
 __version__ = "0.1.0"

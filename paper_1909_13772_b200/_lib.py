@@ -16,10 +16,11 @@ LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
 
 LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
 ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 SRT, TRT, MRT, SRT_FIELD = 0, 1, 2, 3
 MASK_FLUID = 0x1
 MASK_UBB = 0x80000000
+MASK_MOVING = 0x20000000
 
 # every symbol include/lbm_b200.h declares (tests check the export table)
 EXPORTS = (
@@ -27,6 +28,7 @@ EXPORTS = (
     "lbm_fused_step", "lbm_collide_only", "lbm_stream_only", "lbm_moments",
     "lbm_pack_rform", "lbm_unpack_rform", "lbm_fill_equilibrium", "lbm_build_cellmask",
     "lbm_collide_cells", "lbm_equilibrium_cells", "lbm_macroscopic_cells",
+    "lbm_build_moving_masks",
 )
 
 
@@ -48,7 +50,16 @@ class Params(ctypes.Structure):
                 ("shift_fx", ctypes.c_double), ("shift_fy", ctypes.c_double),
                 ("shift_fz", ctypes.c_double), ("ubb", ctypes.c_double * 27),
                 ("pressure", ctypes.c_double * 27), ("mrt", ctypes.c_void_p),
-                ("omega_cells", ctypes.c_void_p)]
+                ("omega_cells", ctypes.c_void_p), ("moving", ctypes.c_void_p)]
+
+
+class Moving(ctypes.Structure):
+    """lbm_moving_t"""
+    _fields_ = [("owner", ctypes.c_void_p), ("linkmask", ctypes.c_void_p),
+                ("bodies", ctypes.c_void_p), ("cell0", ctypes.c_void_p),
+                ("forces", ctypes.c_void_p), ("n_slots", ctypes.c_int),
+                ("blocks", ctypes.c_int * 3), ("block_cells", ctypes.c_int * 3),
+                ("rho0", ctypes.c_double)]
 
 
 _lib = None
@@ -86,6 +97,7 @@ def load(path: Path | None = None):
         "lbm_collide_cells": ([I, PR, P, I64, P], I),
         "lbm_equilibrium_cells": ([I, P, P, P, I64, P], I),
         "lbm_macroscopic_cells": ([I, PR, P, P, P, P, I64, P], I),
+        "lbm_build_moving_masks": ([G, P, P, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -94,8 +106,10 @@ def load(path: Path | None = None):
     if lib.lbm_abi_version() != ABI_VERSION:
         raise BackendError("kernel library ABI mismatch")
     if (lib.lbm_struct_size(0) != ctypes.sizeof(Grid)
-            or lib.lbm_struct_size(1) != ctypes.sizeof(Params)):
-        raise BackendError("lbm_grid_t / lbm_params_t layout differs between include/lbm_b200.h "
+            or lib.lbm_struct_size(1) != ctypes.sizeof(Params)
+            or lib.lbm_struct_size(2) != ctypes.sizeof(Moving)):
+        raise BackendError("lbm_grid_t / lbm_params_t / lbm_moving_t layout differs between "
+                           "include/lbm_b200.h "
                            "and the ctypes mirror")
     _lib = lib
     return lib

@@ -96,6 +96,33 @@ int check_params(const lbm_params_t* p, int q, KParams* k, cudaStream_t s, int r
     if (p->model == LBM_SRT_FIELD && p->force_mode == LBM_FORCE_SHIFT)
         return fail(LBM_EINVAL, "SimpleShift needs an SRT model with one global rate");
     k->omega = p->omega_cells;
+    k->mv_owner = nullptr;
+    k->mv_link = nullptr;
+    k->mv_bodies = k->mv_cell0 = nullptr;
+    k->mv_forces = nullptr;
+    k->mv_slots = k->mv_bx = k->mv_by = 0;
+    k->mv_cx = k->mv_cy = k->mv_cz = 1;
+    k->mv_rho0 = 1.0;
+    if (p->moving) {
+        const lbm_moving_t* m = p->moving;
+        if (!m->owner || !m->linkmask || (!m->bodies && m->n_slots > 0) || !m->cell0)
+            return fail(LBM_EINVAL, "moving walls: NULL array");
+        if (m->n_slots < 0 || m->blocks[0] < 1 || m->blocks[1] < 1 || m->blocks[2] < 1 ||
+            m->block_cells[0] < 1 || m->block_cells[1] < 1 || m->block_cells[2] < 1)
+            return fail(LBM_EINVAL, "moving walls: bad block grid");
+        k->mv_owner = m->owner;
+        k->mv_link = m->linkmask;
+        k->mv_bodies = m->bodies;
+        k->mv_cell0 = m->cell0;
+        k->mv_forces = m->forces;
+        k->mv_slots = m->n_slots;
+        k->mv_bx = m->blocks[0];
+        k->mv_by = m->blocks[1];
+        k->mv_cx = m->block_cells[0];
+        k->mv_cy = m->block_cells[1];
+        k->mv_cz = m->block_cells[2];
+        k->mv_rho0 = m->rho0;
+    }
     if (p->force_mode < 0 || p->force_mode > 3)
         return fail(LBM_EINVAL, "bad force mode %d", p->force_mode);
     if (p->force_mode == LBM_FORCE_SHIFT && p->model != LBM_SRT)
@@ -230,6 +257,41 @@ __global__ void k_build_mask(KGrid g, const uint32_t* __restrict__ flags, MaskBi
     if (n_pr) atomicAdd(&err[6], n_pr);
 }
 
+// combined masks of a moving-body sweep (lbm_build_moving_masks)
+template <int Q>
+__global__ void k_moving_masks(KGrid g, const uint32_t* __restrict__ cm_in,
+                               const int32_t* __restrict__ owner, uint32_t* __restrict__ cm_out,
+                               uint32_t* __restrict__ linkmask, int* n_links) {
+    using D = Dirs<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    const int X = g.nx + 2, Y = g.ny + 2;
+    uint32_t code = cm_in[cell];
+    uint32_t lm = 0;
+    int n = 0;
+    if (owner[((int64_t)(z + 1) * Y + (y + 1)) * X + (x + 1)] >= 0) {
+        code &= ~LBM_MASK_FLUID;          // covered: keeps its static links, skips collision
+    } else if (code & LBM_MASK_FLUID) {
+        static_for<1, Q>([&](auto J_) {
+            constexpr int j = decltype(J_)::value;
+            // pulled direction j reads x - c_j (raw ghost-inclusive neighbour)
+            const int64_t nb = ((int64_t)(z + 1 - D::cz[j]) * Y + (y + 1 - D::cy[j])) * X +
+                               (x + 1 - D::cx[j]);
+            if (owner[nb] >= 0) {
+                lm |= 1u << j;
+                ++n;
+            }
+        });
+        if (lm) code |= lm | LBM_MASK_MOVING;
+    }
+    cm_out[cell] = code;
+    linkmask[cell] = lm;
+    if (n) atomicAdd(n_links, n);
+}
+
 // ------------------------------------------------------------ flat cells
 template <int Q, int MODEL, int FORCE>
 __global__ void k_collide_cells(KParams p, double* __restrict__ f, int64_t n) {
@@ -314,7 +376,8 @@ extern "C" {
 int lbm_abi_version(void) { return LBM_B200_ABI_VERSION; }
 
 size_t lbm_struct_size(int which) {
-    return which == 0 ? sizeof(lbm_grid_t) : which == 1 ? sizeof(lbm_params_t) : 0;
+    return which == 0 ? sizeof(lbm_grid_t)
+                      : which == 1 ? sizeof(lbm_params_t) : which == 2 ? sizeof(lbm_moving_t) : 0;
 }
 
 const char* lbm_last_error(void) { return g_err; }
@@ -480,6 +543,24 @@ int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags, const uint32_
         return cudaGetLastError();
     });
     return cuda_status(e, "lbm_build_cellmask");
+}
+
+int lbm_build_moving_masks(const lbm_grid_t* g, const uint32_t* cellmask_in, const int32_t* owner,
+                           uint32_t* cellmask_out, uint32_t* linkmask, int* n_links, void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!cellmask_in || !owner || !cellmask_out || !linkmask || !n_links)
+        return fail(LBM_EINVAL, "NULL buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    dim3 blk = cell_block(g->nx);
+    dim3 grid((g->nx + blk.x - 1) / blk.x, g->ny, g->nz);
+    cudaError_t e = by_q(g->q, [&](auto Qc) {
+        k_moving_masks<decltype(Qc)::value><<<grid, blk, 0, s>>>(k, cellmask_in, owner, cellmask_out,
+                                                                 linkmask, n_links);
+        return cudaGetLastError();
+    });
+    return cuda_status(e, "lbm_build_moving_masks");
 }
 
 int lbm_collide_cells(int q, const lbm_params_t* p, double* f, int64_t n, void* stream) {

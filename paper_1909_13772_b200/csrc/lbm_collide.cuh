@@ -36,6 +36,14 @@ struct KParams {
     float fcF[27], fguo_p[27], fguo_q[27];
     int mrt_fast;                 // fp32 D3Q27 MRT: factorised raw-moment form
     const double* omega;          // SRT per-cell rates (nz, ny, nx), model 4
+    // moving-body walls (lbm_moving_t), read only on cells with LBM_MASK_MOVING
+    const int* mv_owner;          // (nz+2, ny+2, nx+2) body slot or -1
+    const uint32_t* mv_link;      // (nz, ny, nx) pulled directions from covered cells
+    const double* mv_bodies;      // (blocks * slots, 9) p, v, omega per block's copy
+    const double* mv_cell0;       // (blocks, 3) first-cell centres
+    double* mv_forces;            // (blocks * slots, 6) force, torque accumulators
+    int mv_slots, mv_bx, mv_by, mv_cx, mv_cy, mv_cz;
+    double mv_rho0;
 };
 
 // MRT tables in constant memory: M, Minv, S, G (q <= 27).  One private copy

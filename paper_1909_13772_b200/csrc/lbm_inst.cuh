@@ -24,6 +24,17 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
     if (z1 <= z0) return cudaSuccess;
     dim3 b = cell_block(g.nx);
     dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
+    if (p.mv_link) {
+        // moving-body walls: a separate instantiation, so the standard sweep
+        // keeps its register allocation (3D stencils, SRT/TRT/dense MRT)
+        if constexpr (Q != 9 && MODEL <= 2 && FORCE != 2) {
+            k_fused<Q, LBM_REAL, MODEL, FORCE, true><<<grid, b, 0, s>>>(
+                g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0);
+            return cudaGetLastError();
+        } else {
+            return cudaErrorInvalidValue;
+        }
+    }
     k_fused<Q, LBM_REAL, MODEL, FORCE><<<grid, b, 0, s>>>(g, p, (const LBM_REAL*)src,
                                                          (LBM_REAL*)dst, cm, tmk, z0);
     return cudaGetLastError();
@@ -80,7 +91,7 @@ cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p,
                   void* dst, const uint32_t* cm, const uint32_t* tmk, int z0, int z1,
                   cudaStream_t s) {
     if (model == LBM_SRT_FIELD) model = 4;
-    else if (model == LBM_MRT && p.mrt_fast) model = 3;
+    else if (model == LBM_MRT && p.mrt_fast && !p.mv_link) model = 3;  // moving walls: dense MRT
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         return by_model<Q>(model, force, [&](auto Mc, auto Fc) {

@@ -149,6 +149,81 @@ __device__ __forceinline__ void pressure_links(const KGrid& g, const KParams& p,
     });
 }
 
+// Moving-body walls (coupling/sweep.py:113-143) on the pulled directions of
+// p.mv_link: the link (x, i = opp(j)) points into a covered cell; the pulled
+// value becomes G[x, i] - ((6 w_i) rho0) (c_i . u_w) with u_w the body's
+// surface velocity at the link midpoint x + c_i / 2, in the reference's
+// operation order (fp64, every op rounded); FORCES adds the momentum
+// dp = 2 G[x, i] - corr and its torque to the (block, body) accumulators.
+template <int Q, typename Acc, bool FORCES>
+__device__ __forceinline__ void moving_links(const KGrid& g, const KParams& p, int x, int y, int z,
+                                             int64_t cell, Acc (&f)[Q]) {
+    using D = Dirs<Q>;
+    const uint32_t lm = __ldg(p.mv_link + cell);
+    const int bx = x / p.mv_cx, by = y / p.mv_cy, bz = z / p.mv_cz;
+    const int blk = (bz * p.mv_by + by) * p.mv_bx + bx;
+    const double* c0 = p.mv_cell0 + 3 * blk;
+    const double px = c0[0] + (double)(x - bx * p.mv_cx);
+    const double py = c0[1] + (double)(y - by * p.mv_cy);
+    const double pz = c0[2] + (double)(z - bz * p.mv_cz);
+    const int X = g.nx + 2, Y = g.ny + 2;
+    double fa[3] = {0.0, 0.0, 0.0}, ta[3] = {0.0, 0.0, 0.0};
+    int last = -1;
+    static_for<1, Q>([&](auto J_) {
+        constexpr int j = decltype(J_)::value;
+        constexpr int i = D::opp[j];
+        constexpr double ci0 = D::cx[i], ci1 = D::cy[i], ci2 = D::cz[i];
+        if ((lm >> j) & 1u) {
+            const int slot = __ldg(p.mv_owner + ((int64_t)(z + 1 + D::cz[i]) * Y + (y + 1 + D::cy[i])) * X +
+                                   (x + 1 + D::cx[i]));
+            const int bi = blk * p.mv_slots + slot;
+            const double* b = p.mv_bodies + 9 * bi;
+            const double rx = (px + 0.5 * ci0) - b[0];
+            const double ry = (py + 0.5 * ci1) - b[1];
+            const double rz = (pz + 0.5 * ci2) - b[2];
+            const double uwx = (b[3] + b[7] * rz) - b[8] * ry;
+            const double uwy = (b[4] + b[8] * rx) - b[6] * rz;
+            const double uwz = (b[5] + b[6] * ry) - b[7] * rx;
+            const double cu = (ci0 * uwx + ci1 * uwy) + ci2 * uwz;
+            const double corr = ((6.0 * wt<Q, i>()) * p.mv_rho0) * cu;
+            double fi;
+            if constexpr (std::is_same_v<Acc, double>) fi = f[j];
+            else fi = (double)f[j] + wt<Q, i>();
+            if constexpr (std::is_same_v<Acc, double>) f[j] = fi - corr;
+            else f[j] = (float)((fi - corr) - wt<Q, j>());
+            if constexpr (FORCES) {
+                if (p.mv_forces) {
+                    if (last >= 0 && last != bi) {   // a second body at this cell: flush
+                        double* acc = p.mv_forces + 6 * last;
+                        for (int k = 0; k < 3; ++k) {
+                            atomicAdd(acc + k, fa[k]);
+                            atomicAdd(acc + 3 + k, ta[k]);
+                            fa[k] = ta[k] = 0.0;
+                        }
+                    }
+                    last = bi;
+                    const double dp = 2.0 * fi - corr;
+                    fa[0] += ci0 * dp;
+                    fa[1] += ci1 * dp;
+                    fa[2] += ci2 * dp;
+                    ta[0] += (ry * ci2 - rz * ci1) * dp;
+                    ta[1] += (rz * ci0 - rx * ci2) * dp;
+                    ta[2] += (rx * ci1 - ry * ci0) * dp;
+                }
+            }
+        }
+    });
+    if constexpr (FORCES) {
+        if (last >= 0) {
+            double* acc = p.mv_forces + 6 * last;
+            for (int k = 0; k < 3; ++k) {
+                atomicAdd(acc + k, fa[k]);
+                atomicAdd(acc + 3 + k, ta[k]);
+            }
+        }
+    }
+}
+
 // Load the 19/27/9 pulled populations of cell (x,y,z) with the fused
 // bounce-back substitution R[x,i] = G[x,opp(i)] (- UBB term) for masked
 // directions (boundary.py:163-170).
@@ -190,7 +265,9 @@ __device__ __forceinline__ void pull_offsets(const KGrid& g, int x, int y, int z
 // (3) conversion + the rare UBB / Pressure corrections under one branch.
 // Acc = double: widened populations f (fp64 storage, or fp32 readout);
 // Acc = float (fp32 storage only): the stored centred g = f - w as is.
-template <int Q, typename Real, typename Acc>
+// MV: 0 no moving-body walls (the standard sweep kernels), 1 moving walls
+// without force accumulation (readouts), 2 moving walls + forces (fused step).
+template <int Q, typename Real, typename Acc, int MV = 0>
 __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                                           const Real* __restrict__ src, int x, int y, int z,
                                           uint32_t code, const uint32_t* __restrict__ typemask,
@@ -199,9 +276,10 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                   "fp32 registers only for fp32 storage");
     using D = Dirs<Q>;
     const int64_t own = lidx(g, z, 0, y, x);
-    const bool typed = (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) != 0u;
+    constexpr uint32_t kTyped = LBM_MASK_UBB | LBM_MASK_PRESSURE | (MV ? LBM_MASK_MOVING : 0u);
+    const bool typed = (code & kTyped) != 0u;
     uint2 t = make_uint2(0u, 0u);
-    if (typed) t = __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
+    if (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) t = __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
     Real raw[Q];
     // link: read the own cell's direction k = opp(i) instead (w_k == w_i, so
     // the fp32 zero-centring offset is the same)
@@ -245,6 +323,10 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
             });
         }
         if (t.y) pressure_links<Q, Real, Acc>(g, p, src, own, t.y, f);
+        if constexpr (MV != 0) {
+            if (code & LBM_MASK_MOVING)
+                moving_links<Q, Acc, MV == 2>(g, p, x, y, z, ((int64_t)z * g.ny + y) * g.nx + x, f);
+        }
     }
 }
 
@@ -299,7 +381,7 @@ __device__ __forceinline__ void store_any(Real* p, Acc v) {
     else *p = v;  // already centred fp32
 }
 
-template <int Q, typename Real, int MODEL, int FORCE>
+template <int Q, typename Real, int MODEL, int FORCE, bool MOVING = false>
 __global__ void __launch_bounds__(128, fused_minb<Q, Real, MODEL>())
     k_fused(KGrid g, KParams p, const Real* __restrict__ src,
                                                Real* __restrict__ dst,
@@ -320,7 +402,7 @@ __global__ void __launch_bounds__(128, fused_minb<Q, Real, MODEL>())
     const uint32_t code = __ldg(cellmask + cell);
     using Acc = AccOf<Real>;
     Acc f[Q];
-    pull_cell<Q, Real, Acc>(g, p, src, x, y, z, code, typemask, generic, f);
+    pull_cell<Q, Real, Acc, MOVING ? 2 : 0>(g, p, src, x, y, z, code, typemask, generic, f);
     if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p, cell);
     Real* dp = opaque(dst + lidx(g, z, 0, y, x));
     static_for<0, Q>([&](auto I_) {
@@ -370,7 +452,7 @@ __global__ void __launch_bounds__(128) k_stream_only(KGrid g, KParams p, const R
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
     const uint32_t code = cellmask[cell];
     double f[Q];
-    pull_cell<Q, Real, double>(g, p, src, x, y, z, code, typemask, true, f);
+    pull_cell<Q, Real, double, 1>(g, p, src, x, y, z, code, typemask, true, f);
     const int64_t n = (int64_t)g.nx * g.ny * g.nz;
 #pragma unroll
     for (int i = 0; i < Q; ++i) out[(int64_t)i * n + cell] = f[i];
@@ -391,7 +473,7 @@ __global__ void __launch_bounds__(128) k_moments(KGrid g, KParams p, const Real*
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
     double f[Q];
     if (stream_form) {
-        pull_cell<Q, Real, double>(g, p, src, x, y, z, cellmask[cell], typemask, true, f);
+        pull_cell<Q, Real, double, 1>(g, p, src, x, y, z, cellmask[cell], typemask, true, f);
     } else {
         const int64_t own = lidx(g, z, 0, y, x);
         static_for<0, Q>([&](auto I_) {

@@ -21,6 +21,10 @@ class NumericsError(BlocksimError):
     """Non-positive density / divergence (errors.py:44)."""
 
 
+class SyncError(BlocksimError):
+    """Distributed body state is inconsistent (errors.py:40)."""
+
+
 class TypeTagError(BlocksimError):
     """A debug type tag or wire dtype code did not match (errors.py:20)."""
 

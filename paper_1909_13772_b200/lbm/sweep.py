@@ -138,8 +138,8 @@ class PdfField:
             for k in range(self.stencil.q):
                 kp.struct.pressure[k] = 2.0 * self.stencil.weights[k] * handling.pressure_density
         s = kp.struct
-        # (struct minus its two trailing pointers, MRT tables)
-        key = (bytes(memoryview(s))[:-16], b"" if kp.tables is None else kp.tables.tobytes())
+        # (struct minus its three trailing pointers, MRT tables)
+        key = (bytes(memoryview(s))[:-24], b"" if kp.tables is None else kp.tables.tobytes())
         # keep the objects alive so their ids cannot be reused
         self._kp_cache[ck] = ((model, force, handling), kp, key)
         return kp, key

@@ -133,6 +133,13 @@ def reference_api():
     ns.make_raw_mrt = make_raw_mrt
     from blocksim.field import write_vtk
     ns.write_vtk = write_vtk
+    import blocksim.coupling as C
+    import blocksim.rpd as R
+    for name in ("map_bodies", "moving_boundary_sweep", "reduce_hydrodynamic_forces",
+                 "reinitialize_uncovered", "covered_cell_counts", "CoupledSystem"):
+        setattr(ns, name, getattr(C, name))
+    for name in ("register_bodies", "add_sphere", "sync_bodies", "local_bodies"):
+        setattr(ns, name, getattr(R, name))
     return ns
 
 
@@ -144,6 +151,10 @@ def b200_api():
     ns.gather_slice = P.gather_slice
     ns.make_raw_mrt = lambda st, shear, other: P.lbm.MRT.raw_moments(st, shear, other)
     ns.write_vtk = P.write_vtk
+    for name in ("map_bodies", "moving_boundary_sweep", "reduce_hydrodynamic_forces",
+                 "reinitialize_uncovered", "covered_cell_counts", "CoupledSystem",
+                 "register_bodies", "add_sphere", "sync_bodies", "local_bodies"):
+        setattr(ns, name, getattr(P, name))
     return ns
 
 
@@ -475,3 +486,70 @@ def oracle_run(spec, oracle):
         done = s
         out[s] = dom.rform()
     return {"pdf": out, "domain": dom}
+
+
+# -------------------------------------------------- moving bodies (row f2)
+COUPLING_CASES = {
+    # a translating + rotating sphere and one straddling the periodic corner,
+    # TRT + Guo, bodies displaced every step (coverage changes: re-collision
+    # of the stored state, uncovered-cell reinitialisation), 2x2x2 blocks
+    "moving_spheres": dict(stencil="D3Q19", dims=(16, 16, 16), root_dims=(2, 2, 2),
+                           model=("TRT_magic", 1.6), force=("Guo", (2e-5, 0.0, -1e-5)),
+                           bodies=[((8.2, 8.1, 7.9), 3.0, 100.0, (0.08, -0.05, 0.03),
+                                    (0.0, 0.003, 0.001)),
+                                   ((1.3, 14.6, 15.4), 2.5, 50.0, (-0.06, 0.07, 0.09),
+                                    (0.002, 0.0, -0.004))],
+                           steps=8, move=True, layout="fzyx"),
+    # stationary body, SRT: equals a NoSlip obstacle (test_coupling.py:236-265)
+    "static_sphere_srt": dict(stencil="D3Q19", dims=(16, 16, 16), root_dims=(1, 1, 1),
+                              model=("SRT", 1.6), force=None,
+                              bodies=[((8.2, 8.1, 7.9), 3.0, 1.0, (0.0, 0.0, 0.0),
+                                       (0.0, 0.0, 0.0))],
+                              steps=12, move=False, layout="zyxf"),
+}
+
+
+def coupling_velocity(x, y, z):
+    return (0.02 * np.sin(2 * np.pi * z / 16.0), 0.01 * np.cos(2 * np.pi * x / 16.0), 0.0 * x)
+
+
+def run_coupling_case(api, ctx, spec, *, pdf_kwargs=None):
+    """The coupled step spelled out with the public functions (system.py:
+    164-196 with the DEM substeps replaced by a prescribed displacement
+    x += v per step): map -> moving_boundary_sweep -> reduce -> move ->
+    sync_bodies -> remap -> reinitialize_uncovered.  Returns (rank 0) the
+    final PDFs, per-step record forces/torques, final body forces, uncovered
+    and link counts."""
+    st = getattr(api, spec["stencil"])
+    nx, ny, nz = spec["dims"]
+    R = spec["root_dims"]
+    forest = api.create_forest(ctx, (0, 0, 0, nx, ny, nz), R, periodic=(True, True, True),
+                               cells_per_block=(nx // R[0], ny // R[1], nz // R[2]))
+    pdf = api.PdfField(forest, st, layout=spec["layout"], **(pdf_kwargs or {}))
+    api.register_bodies(forest, contact_threshold=1.0)
+    for pos, r, m, v, w in spec["bodies"]:
+        api.add_sphere(forest, pos, r, mass=m, velocity=v, angular_velocity=w)
+    api.sync_bodies(forest)
+    api.fill_equilibrium(pdf, 1.0, coupling_velocity)
+    model = model_of(api, spec, st)
+    force = force_of(api, spec)
+    mapping = api.map_bodies(forest, st)
+    out = {"records": [], "uncovered": [], "links": []}
+    for _ in range(spec["steps"]):
+        out["links"].append(sum(mapping.link_count(b.id) for b in forest.local_blocks()))
+        records = api.moving_boundary_sweep(pdf, model, mapping, force=force)
+        out["records"].append([(r[3], tuple(float(v) for v in r[5]), tuple(float(v) for v in r[6]))
+                               for r in records])
+        api.reduce_hydrodynamic_forces(forest, records)
+        if spec["move"]:
+            for b in api.local_bodies(forest):
+                b.position = b.position + b.linear_velocity
+        api.sync_bodies(forest)
+        new = api.map_bodies(forest, st)
+        out["uncovered"].append(api.reinitialize_uncovered(pdf, mapping, new))
+        mapping = new
+    out["pdf"] = api.gather_slice(forest, "pdf", (0, 0, 0), forest.global_cells(0))
+    out["bodies"] = [(b.uid, tuple(b.position), tuple(b.hydrodynamic_force),
+                      tuple(b.hydrodynamic_torque)) for b in api.local_bodies(forest)]
+    out["covered"] = api.covered_cell_counts(forest, mapping)
+    return out if ctx.rank == 0 else None

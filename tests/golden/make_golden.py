@@ -106,6 +106,23 @@ def make_snapshot():
     print("snapshot:", len(res["image"]), "bytes,", len(res["vtk"]), "vtk files")
 
 
+def make_coupling():
+    """Row f2: the reference's coupled steps (cases.COUPLING_CASES) - final
+    PDFs as arrays, forces/counts as JSON."""
+    meta = json.loads((HERE / "digests.json").read_text())
+    meta["coupling"] = {}
+    for name, spec in cases.COUPLING_CASES.items():
+        api = cases.reference_api()
+        res = SimRuntime(1, seed=0).run(lambda ctx: cases.run_coupling_case(api, ctx, spec))[0]
+        np.savez(HERE / f"coupling_{name}.npz", pdf=res["pdf"])
+        meta["coupling"][name] = {"records": res["records"], "uncovered": res["uncovered"],
+                                  "links": res["links"], "bodies": res["bodies"],
+                                  "covered": {str(k): v for k, v in res["covered"].items()},
+                                  "pdf": sha(res["pdf"])}
+        print("coupling", name, res["links"], res["uncovered"], flush=True)
+    (HERE / "digests.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
+
+
 def make_units():
     """Reference unit functions on seeded random cells."""
     import blocksim.lbm as L
@@ -157,7 +174,10 @@ if __name__ == "__main__":
     args = sys.argv[1:]
     if args == ["snapshot"]:
         make_snapshot()
+    elif args == ["coupling"]:
+        make_coupling()
     else:
         main(args or None)
         if not args:
             make_snapshot()
+            make_coupling()
