@@ -18,11 +18,16 @@ inline dim3 cell_block(int nx) {
     return dim3(bx, 1, 1);
 }
 
+inline dim3 fused_block(int nx) {
+    int bx = nx >= LBM_FUSED_BX ? LBM_FUSED_BX : ((nx + 31) / 32) * 32;
+    return dim3(bx, 1, 1);
+}
+
 template <int Q, int MODEL, int FORCE>
 cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst,
                     const uint32_t* cm, const uint32_t* tmk, int z0, int z1, cudaStream_t s) {
     if (z1 <= z0) return cudaSuccess;
-    dim3 b = cell_block(g.nx);
+    dim3 b = fused_block(g.nx);
     dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
     if (p.mv_link) {
         // moving-body walls: a separate instantiation, so the standard sweep

@@ -381,8 +381,20 @@ __device__ __forceinline__ void store_any(Real* p, Acc v) {
     else *p = v;  // already centred fp32
 }
 
+// threads per block of the fused kernel (x extent of a block's row segment).
+// Measured on B200 (config 4 / 3 / 2): 64 and 128 equal within noise, 256 -1..-9 %,
+// 512 -12..-25 % (fewer resident blocks, coarser tail).
+#ifndef LBM_FUSED_BX
+#define LBM_FUSED_BX 128
+#endif
+template <int Q, typename Real, int MODEL>
+constexpr int fused_minb_bx() {
+    constexpr int m = fused_minb<Q, Real, MODEL>() * 128 / LBM_FUSED_BX;
+    return m < 1 ? 1 : m;
+}
+
 template <int Q, typename Real, int MODEL, int FORCE, bool MOVING = false>
-__global__ void __launch_bounds__(128, fused_minb<Q, Real, MODEL>())
+__global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
     k_fused(KGrid g, KParams p, const Real* __restrict__ src,
                                                Real* __restrict__ dst,
                                                const uint32_t* __restrict__ cellmask,

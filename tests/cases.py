@@ -513,13 +513,13 @@ def coupling_velocity(x, y, z):
     return (0.02 * np.sin(2 * np.pi * z / 16.0), 0.01 * np.cos(2 * np.pi * x / 16.0), 0.0 * x)
 
 
-def run_coupling_case(api, ctx, spec, *, pdf_kwargs=None):
+def run_coupling_case(api, ctx, spec, *, pdf_kwargs=None, all_ranks=False):
     """The coupled step spelled out with the public functions (system.py:
     164-196 with the DEM substeps replaced by a prescribed displacement
     x += v per step): map -> moving_boundary_sweep -> reduce -> move ->
     sync_bodies -> remap -> reinitialize_uncovered.  Returns (rank 0) the
     final PDFs, per-step record forces/torques, final body forces, uncovered
-    and link counts."""
+    and link counts (this rank's; all_ranks=True returns them on every rank)."""
     st = getattr(api, spec["stencil"])
     nx, ny, nz = spec["dims"]
     R = spec["root_dims"]
@@ -552,4 +552,4 @@ def run_coupling_case(api, ctx, spec, *, pdf_kwargs=None):
     out["bodies"] = [(b.uid, tuple(b.position), tuple(b.hydrodynamic_force),
                       tuple(b.hydrodynamic_torque)) for b in api.local_bodies(forest)]
     out["covered"] = api.covered_cell_counts(forest, mapping)
-    return out if ctx.rank == 0 else None
+    return out if (ctx.rank == 0 or all_ranks) else None
