@@ -35,6 +35,11 @@
  *                       (coupling/mapping.py:133-150) for moving_boundary_sweep
  *                       (coupling/sweep.py:45-155; the wall rule itself is
  *                       fused into lbm_fused_step through lbm_params_t.moving).
+ *   lbm_fused_step_peer lbm_fused_step with the per-step z-face exchange
+ *                       (field/ghost.py:202-264) fused in: boundary planes
+ *                       store their crossing directions into the
+ *                       neighbour's ghost plane (peer HBM over NVLink);
+ *                       lbm_stream_signal / lbm_stream_wait order the phases.
  *   lbm_face_span       geometry of the per-step z-face ghost exchange
  *                       (field/ghost.py:112-173,202-264), restricted to the
  *                       PDF directions that cross the face.
@@ -59,7 +64,7 @@
 extern "C" {
 #endif
 
-#define LBM_B200_ABI_VERSION 3
+#define LBM_B200_ABI_VERSION 4
 
 /* status codes */
 #define LBM_OK 0
@@ -187,6 +192,37 @@ int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p,
                    const void* src, void* dst, const uint32_t* cellmask,
                    const uint32_t* typemask, int z_begin, int z_end,
                    void* stream);
+
+/* lbm_fused_step plus the fused z-face halo (ABI 4): the plane z = 0 also
+ * stores its c_z = -1 directions into peer_lo, the plane z = nz-1 its
+ * c_z = +1 directions into peer_hi, at the same (slot, y, x) offsets.  A peer
+ * pointer is the z-block of the neighbour's receiving ghost plane (its field
+ * base + lbm_ghost_block_offset(neighbour grid, face facing us)); it may live
+ * in this GPU's memory or in a peer GPU's HBM mapped through CUDA IPC over
+ * NVLink.  NULL: that face is not written.  Replaces the per-step
+ * exchange_ghosts of stream_collide (lbm/sweep.py:110-114,
+ * field/ghost.py:202-264) for the directions that cross the face. */
+int lbm_fused_step_peer(const lbm_grid_t* g, const lbm_params_t* p,
+                        const void* src, void* dst, const uint32_t* cellmask,
+                        const uint32_t* typemask, int z_begin, int z_end,
+                        void* peer_lo, void* peer_hi, void* stream);
+
+/* Element offset from a field base to the z-block (all q slots) of its ghost
+ * plane on `face` (0: z = -1, 1: z = nz) - the target of a neighbour's
+ * lbm_fused_step_peer stores. */
+int lbm_ghost_block_offset(const lbm_grid_t* g, int face, int64_t* offset);
+
+/* Stream-ordered 32-bit flags for the fused halo's phase protocol (ABI 4).
+ * signal: after all earlier work of `stream` (with a memory barrier), write
+ * `value` to the device word `flag` (local, or a peer's mapped word).
+ * wait: later work of `stream` starts once (int32)(*flag - value) >= 0.
+ * Both are driver stream memory operations: nothing spins on an SM. */
+int lbm_stream_signal(void* flag, uint32_t value, void* stream);
+/* Stream-ordered copy of `bytes` between any two device addresses (own HBM,
+ * a peer GPU's mapped HBM): the fused halo's full-run copy after
+ * lbm_collide_only. */
+int lbm_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+int lbm_stream_wait(const void* flag, uint32_t value, void* stream);
 
 /* Collide, in place, every interior cell whose cellmask has LBM_MASK_FLUID
  * (G_0 = C(R_0)). */

@@ -10,7 +10,7 @@ with a zero-copy NCCL halo of the crossing directions.
 """
 from .errors import BackendError, BlocksimError, BufferUnderflowError, NumericsError, \
     SyncError, TopologyError, TypeTagError, ValidationError
-from .runtime import Context, init_distributed, run
+from .runtime import Context, ThreadContext, init_distributed, run
 from .blockforest import BlockForest, BlockId, create_forest
 from .field import Field, FieldDataHandler, FlagField, FlagFieldHandler, GhostPackInfo, \
     exchange_ghosts, gather_slice, sweep

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
 
 LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
 ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
-ABI_VERSION = 3
+ABI_VERSION = 4
 SRT, TRT, MRT, SRT_FIELD = 0, 1, 2, 3
 MASK_FLUID = 0x1
 MASK_UBB = 0x80000000
@@ -28,7 +28,8 @@ EXPORTS = (
     "lbm_fused_step", "lbm_collide_only", "lbm_stream_only", "lbm_moments",
     "lbm_pack_rform", "lbm_unpack_rform", "lbm_fill_equilibrium", "lbm_build_cellmask",
     "lbm_collide_cells", "lbm_equilibrium_cells", "lbm_macroscopic_cells",
-    "lbm_build_moving_masks",
+    "lbm_build_moving_masks", "lbm_fused_step_peer", "lbm_ghost_block_offset",
+    "lbm_stream_signal", "lbm_stream_wait", "lbm_copy_async",
 )
 
 
@@ -98,6 +99,11 @@ def load(path: Path | None = None):
         "lbm_equilibrium_cells": ([I, P, P, P, I64, P], I),
         "lbm_macroscopic_cells": ([I, PR, P, P, P, P, I64, P], I),
         "lbm_build_moving_masks": ([G, P, P, P, P, P, P], I),
+        "lbm_fused_step_peer": ([G, PR, P, P, P, P, I, I, P, P, P], I),
+        "lbm_ghost_block_offset": ([G, I, ctypes.POINTER(I64)], I),
+        "lbm_stream_signal": ([P, ctypes.c_uint32, P], I),
+        "lbm_stream_wait": ([P, ctypes.c_uint32, P], I),
+        "lbm_copy_async": ([P, P, I64, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -9,6 +9,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <cuda.h>
+
 #include "../../include/lbm_b200.h"
 #include "lbm_kernels.cuh"
 #include "lbm_launch.h"
@@ -103,6 +105,7 @@ int check_params(const lbm_params_t* p, int q, KParams* k, cudaStream_t s, int r
     k->mv_slots = k->mv_bx = k->mv_by = 0;
     k->mv_cx = k->mv_cy = k->mv_cz = 1;
     k->mv_rho0 = 1.0;
+    k->peer_lo = k->peer_hi = nullptr;
     if (p->moving) {
         const lbm_moving_t* m = p->moving;
         if (!m->owner || !m->linkmask || (!m->bodies && m->n_slots > 0) || !m->cell0)
@@ -439,6 +442,105 @@ int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p, const void* src, 
                         : unit_f32::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
                                           typemask, z_begin, z_end, s);
     return cuda_status(e, "lbm_fused_step");
+}
+
+int lbm_fused_step_peer(const lbm_grid_t* g, const lbm_params_t* p, const void* src, void* dst,
+                        const uint32_t* cellmask, const uint32_t* typemask, int z_begin,
+                        int z_end, void* peer_lo, void* peer_hi, void* stream) {
+    KGrid k;
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
+    if (!src || !dst || !cellmask || !typemask) return fail(LBM_EINVAL, "NULL buffer");
+    if (src == dst) return fail(LBM_EINVAL, "fused step needs two fields (src != dst)");
+    if (z_begin < 0 || z_end > g->nz || z_begin > z_end)
+        return fail(LBM_EINVAL, "plane range [%d, %d) outside 0..%d", z_begin, z_end, g->nz);
+    if (peer_lo && g->zface_lo != LBM_ZFACE_HALO)
+        return fail(LBM_EINVAL, "peer_lo given but the low z face is not a halo face");
+    if (peer_hi && g->zface_hi != LBM_ZFACE_HALO)
+        return fail(LBM_EINVAL, "peer_hi given but the high z face is not a halo face");
+    if (g->q == 9 && (peer_lo || peer_hi)) return fail(LBM_EINVAL, "D2Q9 has no z faces");
+    kp.peer_lo = peer_lo;
+    kp.peer_hi = peer_hi;
+    cudaError_t e = g->real_bytes == 8
+                        ? unit_f64::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
+                                          typemask, z_begin, z_end, s)
+                        : unit_f32::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
+                                          typemask, z_begin, z_end, s);
+    return cuda_status(e, "lbm_fused_step_peer");
+}
+
+int lbm_ghost_block_offset(const lbm_grid_t* g, int face, int64_t* offset) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (face != 0 && face != 1) return fail(LBM_EINVAL, "face must be 0 (low z) or 1 (high z)");
+    if (!offset) return fail(LBM_EINVAL, "offset is NULL");
+    *offset = face == 0 ? 0 : (int64_t)(g->nz + 1) * k.zstride;
+    return LBM_OK;
+}
+
+// Stream-ordered flag signalling for the fused halo (driver stream memory
+// operations, resolved at run time so the library needs no -lcuda).  A wait
+// blocks the stream's front end, never an SM.
+namespace {
+typedef CUresult (*pfn_write_t)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*pfn_wait_t)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+pfn_write_t g_write32 = nullptr;
+pfn_wait_t g_wait32 = nullptr;
+int g_flush_ok = -1;
+
+int memops_init() {
+    if (g_write32 && g_wait32) return LBM_OK;
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* w = nullptr;
+    void* v = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess || !w)
+        return fail(LBM_ECUDA, "driver entry point cuStreamWriteValue32 unavailable");
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) != cudaSuccess ||
+        q2 != cudaDriverEntryPointSuccess || !v)
+        return fail(LBM_ECUDA, "driver entry point cuStreamWaitValue32 unavailable");
+    g_write32 = (pfn_write_t)w;
+    g_wait32 = (pfn_wait_t)v;
+    int dev = 0, flush = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, dev) == cudaSuccess)
+        g_flush_ok = flush ? 1 : 0;
+    else
+        g_flush_ok = 0;
+    return LBM_OK;
+}
+}  // namespace
+
+int lbm_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+    if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(LBM_EINVAL, "bad copy");
+    if (bytes == 0) return LBM_OK;
+    return cuda_status(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream),
+                       "lbm_copy_async");
+}
+
+int lbm_stream_signal(void* flag, uint32_t value, void* stream) {
+    if (!flag) return fail(LBM_EINVAL, "flag is NULL");
+    int st = memops_init();
+    if (st != LBM_OK) return st;
+    // default flags: a memory barrier orders every earlier write of the
+    // stream (the fused kernel's peer stores) before the flag write
+    CUresult r = g_write32((CUstream)stream, (CUdeviceptr)flag, (cuuint32_t)value, 0);
+    if (r != CUDA_SUCCESS) return fail(LBM_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    return LBM_OK;
+}
+
+int lbm_stream_wait(const void* flag, uint32_t value, void* stream) {
+    if (!flag) return fail(LBM_EINVAL, "flag is NULL");
+    int st = memops_init();
+    if (st != LBM_OK) return st;
+    unsigned int fl = CU_STREAM_WAIT_VALUE_GEQ | (g_flush_ok == 1 ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+    CUresult r = g_wait32((CUstream)stream, (CUdeviceptr)flag, (cuuint32_t)value, fl);
+    if (r != CUDA_SUCCESS) return fail(LBM_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    return LBM_OK;
 }
 
 int lbm_collide_only(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,

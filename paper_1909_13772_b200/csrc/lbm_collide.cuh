@@ -44,6 +44,11 @@ struct KParams {
     double* mv_forces;            // (blocks * slots, 6) force, torque accumulators
     int mv_slots, mv_bx, mv_by, mv_cx, mv_cy, mv_cz;
     double mv_rho0;
+    // fused z-face halo (lbm_fused_step_peer): the z-block (all q slots) of
+    // the lower / upper neighbour's receiving ghost plane, in its own memory
+    // (same device, or a peer GPU's HBM mapped over NVLink); NULL otherwise
+    void* peer_lo;
+    void* peer_hi;
 };
 
 // MRT tables in constant memory: M, Minv, S, G (q <= 27).  One private copy

@@ -421,6 +421,25 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
         constexpr int i = decltype(I_)::value;
         store_any<Q, i>(dp + g.dslot[i], f[i]);
     });
+    // Fused halo: a boundary plane also writes the directions that leave the
+    // box through its face straight into the neighbour's ghost plane (peer
+    // HBM over NVLink, or another slab on this device) - the per-step
+    // exchange of field/ghost.py:202-264 without a separate send/recv.
+    // Block-uniform (z is per block), so interior planes pay one test.
+    if (z == 0 && p.peer_lo != nullptr) {
+        Real* pp = opaque(static_cast<Real*>(p.peer_lo) + (int64_t)(y + 1) * g.pitch + g.xoff + x);
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            if constexpr (D::cz[i] == -1) store_any<Q, i>(pp + g.dslot[i], f[i]);
+        });
+    }
+    if (z == g.nz - 1 && p.peer_hi != nullptr) {
+        Real* pp = opaque(static_cast<Real*>(p.peer_hi) + (int64_t)(y + 1) * g.pitch + g.xoff + x);
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            if constexpr (D::cz[i] == 1) store_any<Q, i>(pp + g.dslot[i], f[i]);
+        });
+    }
 }
 
 // G_0 = C(R_0): collide fluid interior cells in place.

@@ -9,10 +9,11 @@ the per-step schedule:
   (what `pdf.src(block)` holds after n sweeps, lbm/sweep.py:93-151) is
   recovered on demand as S(G_{n-1}) from the swapped-out buffer;
 * P = 1: one fused launch per step (periodic z wraps in the kernel);
-* P > 1: boundary planes first on a high-priority stream, their crossing
-  directions sent zero-copy to the z-neighbours (NCCL send/recv straight
-  from / into the field), the interior planes computed concurrently on the
-  caller's stream.
+* P > 1: boundary planes first on a high-priority stream, the interior
+  planes concurrently on the caller's stream.  The boundary kernel stores
+  its crossing directions straight into the z-neighbours' ghost planes
+  (halo.PeerHalo: peer HBM over NVLink, ordered by stream flags); where the
+  ranks cannot map each other they go out by zero-copy NCCL send/recv.
 
 Host<->device traffic happens only on upload (host R-form written by the
 user), readout (host arrays touched) and mask builds; never inside the step.
@@ -376,9 +377,11 @@ class DeviceLattice:
 
     @property
     def halo(self):
+        """z-face transport (collective on first use): the fused peer-store
+        halo where the ranks can map each other, else NCCL / gloo-staged."""
         if self._halo is None:
-            from .halo import Halo
-            self._halo = Halo(self)
+            from .halo import make_halo
+            self._halo = make_halo(self)
         return self._halo
 
     def ensure_collided(self, kp, key, masks):
@@ -408,7 +411,11 @@ class DeviceLattice:
         _lib.call("lbm_collide_only", self.gref, kp.ref, _lib.ptr(self.buf[self.cur]),
                   _lib.ptr(masks.cellmask), self._sp())
         if self.has_halo:
-            self.halo.exchange(self.buf[self.cur], self.stream)
+            # on the boundary stream, ordered after the collide (main)
+            sb = self._streams_get()["boundary"]
+            sb.wait_stream(self.stream)
+            self.halo.after_collide(self, sb)
+            self.stream.wait_stream(sb)
         self.cur_kind = "G"
         self.coll_key = key
 
@@ -447,7 +454,7 @@ class DeviceLattice:
                     _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst),
                               cm, tm, 0, nz, self._sp(main))
             else:
-                self._halo_step(kp, src, dst, cm, tm, main, first=(n == 0))
+                self._halo_step(kp, src, dst, cm, tm, main)
             self.cur = 1 - self.cur
             self.prev_kind = "G"
             self.steps += 1
@@ -487,23 +494,23 @@ class DeviceLattice:
         self.stream.wait_stream(side)
         return self._graphs[(key, self.cur)][0]
 
-    def _halo_step(self, kp, src, dst, cm, tm, main, first):
+    def _halo_step(self, kp, src, dst, cm, tm, main):
         """One overlapped step: B(n) = boundary planes on the high-priority
-        stream followed by the zero-copy halo send/recv, I(n) = interior
+        stream, its crossing directions handed to the halo transport (fused
+        peer stores or send/recv), I(n) = interior
         planes on the caller's stream.  Hazards: B(n) after I(n-1) (B writes
         planes I(n-1) reads); I(n) after B(n-1) (I writes planes B(n-1)
         reads); B(n+1) after the halo of step n (stream order)."""
         S = self._streams_get()
         sb = S["boundary"]
         nz = self.box.nz
-        if not first:
-            main.wait_event(S["ev_b"])       # I(n) after B(n-1)
-            sb.wait_event(S["ev_i"])         # B(n) after I(n-1)
-        for z in sorted({0, nz - 1}):
-            _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
-                      z, z + 1, self._sp(sb))
+        # also across stream_collide calls (one sweep per call is the common
+        # case); waiting on a never-recorded event is a no-op
+        main.wait_event(S["ev_b"])           # I(n) after B(n-1)
+        sb.wait_event(S["ev_i"])             # B(n) after I(n-1)
+        self.halo.boundary(self, kp, src, dst, cm, tm, sb)
         S["ev_b"].record(sb)
-        self.halo.exchange(dst, sb)
+        self.halo.after_boundary(self, dst, sb)
         if nz > 2:
             _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
                       1, nz - 1, self._sp(main))

@@ -17,11 +17,21 @@ peer's low-face send lands in my high ghost plane and vice versa.
 
 The transport only slices tensors and calls torch.distributed, so the same
 code runs on CPU tensors over gloo in the world_size-2 tests.
+
+`PeerHalo` is the B200-native transport: the boundary-plane kernel itself
+stores the crossing directions into the neighbour's ghost plane
+(lbm_fused_step_peer) - in the neighbour's HBM, mapped through CUDA IPC over
+NVLink / NVSwitch, or directly when the ranks share a process - so the halo
+moves while the plane is computed and no collective runs at all.  `make_halo`
+picks it whenever every rank can map its neighbours; NCCL send/recv (`Halo`)
+stays as the fallback transport.
 """
 from __future__ import annotations
 
 import ctypes
+import os
 
+import torch
 import torch.distributed as dist
 
 from . import _lib
@@ -92,13 +102,32 @@ def run_ops(ops, flat, group=None):
 
 
 class Halo:
-    """Exchange plan of one DeviceLattice."""
+    """Exchange plan of one DeviceLattice (NCCL send/recv, or gloo-staged)."""
+
+    kind = "nccl"
 
     def __init__(self, lattice):
         box = lattice.box
         self.spans = face_spans(lattice.gref)
         self.ops = plan_ops(box.zface_lo, box.zface_hi, box.lo_peer, box.hi_peer, self.spans)
         self.bytes_per_exchange = sum(c for k, _, _, c in self.ops if k == "send") * lattice.real_bytes
+        if lattice.device.type == "cuda" and dist.is_initialized() and dist.get_backend() != "nccl":
+            self.kind = "staged"
+
+    def after_collide(self, lat, stream):
+        """G_0's crossing directions -> the neighbours' ghost planes."""
+        self.exchange(lat.buf[lat.cur], stream)
+
+    def boundary(self, lat, kp, src, dst, cm, tm, stream):
+        """B(n): the boundary planes, then the halo of their crossing runs."""
+        nz = lat.box.nz
+        for z in sorted({0, nz - 1}):
+            _lib.call("lbm_fused_step", lat.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
+                      z, z + 1, _lib.stream_ptr(stream))
+        return stream
+
+    def after_boundary(self, lat, dst, stream):
+        self.exchange(dst, stream)
 
     def exchange(self, flat, stream):
         """Fill the ghost planes of `flat` from the neighbours' boundary
@@ -109,3 +138,187 @@ class Halo:
             works = run_ops(self.ops, flat)
             for w in works:
                 w.wait()
+
+
+# ------------------------------------------------------------ fused halo
+def _face_geometry(lat):
+    """(send_off, count) per face and the receiving ghost-block offsets."""
+    spans = face_spans(lat.gref)
+    blocks = {}
+    for face in (0, 1):
+        off = ctypes.c_int64()
+        _lib.call("lbm_ghost_block_offset", lat.gref, face, ctypes.byref(off))
+        blocks[face] = off.value
+    return spans, blocks
+
+
+class PeerHalo:
+    """Fused peer-store z-face halo with a device-side phase protocol.
+
+    Every rank publishes its two PDF buffers and a two-word flag array
+    (from_lo, from_hi) to its z-neighbours.  Rank r's step n then runs, on its
+    boundary stream:
+
+      1. phase entry k: write k into the neighbours' flag words (a stream
+         memory op, ordered after all earlier work of the stream - including
+         the previous phase's peer stores and, through the wait on the main
+         stream, every readout), then wait until both own flag words are
+         >= k.  Rank and neighbour have now both finished phase k-1 and all
+         reads of the buffers phase k writes into;
+      2. the boundary planes with lbm_fused_step_peer: each plane also stores
+         its crossing directions into the neighbour's dst ghost plane.
+
+    After collide_only (G_0) a phase copies the whole crossing runs (x/y
+    ghost ring included, like the NCCL transport) instead.
+
+    mode "device": flags + memops (one process per GPU over NVLink, or the
+    in-process thread ranks).  mode "host": ranks are processes sharing one
+    GPU; the phase entry is a device synchronize + a host barrier instead of
+    stream waits, because processes time-sliced on one GPU must not wait on
+    each other on the device (B200_PROFILING: Xid 109).  Peers in another
+    process are opened from CUDA IPC handles (torch.multiprocessing's
+    reduction); in-process peers are used directly."""
+
+    def __init__(self, lat, mode: str):
+        self.kind = "peer-" + mode
+        self.mode = mode
+        self.lat = lat
+        box = lat.box
+        ctx = lat.ctx
+        self.spans, self.blocks = _face_geometry(lat)
+        self.flags = torch.zeros(2, dtype=torch.int32, device=lat.device)
+        # the zero fill must land before any neighbour can signal into it
+        torch.cuda.current_stream(lat.device).synchronize()
+        self.phase = 0
+        in_process = getattr(ctx, "backend", None) == "threads"
+        self.lockstep = in_process
+        if in_process:
+            key = ("peer-halo", id(lat.forest.ctx.group), lat.pdf.key)
+            table = ctx.group.shared.setdefault(key, {})
+            table[ctx.rank] = (lat.buf[0], lat.buf[1], self.flags)
+            mine = None
+        else:
+            from torch.multiprocessing.reductions import reduce_tensor
+            mine = tuple(reduce_tensor(t) for t in (lat.buf[0], lat.buf[1], self.flags))
+        info = {"handles": mine, "spans": self.spans, "blocks": self.blocks,
+                "pitch": lat.grid.pitch, "rb": lat.real_bytes, "q": lat.q}
+        peers = ctx.all_gather(info)
+        self.peer = {}          # face -> (buf0, buf1, flags) of the neighbour across it
+        self.peer_info = {}
+        for face, peer, facing in ((0, box.lo_peer, 1), (1, box.hi_peer, 0)):
+            zmode = box.zface_lo if face == 0 else box.zface_hi
+            if zmode != _lib.ZFACE_HALO:
+                continue
+            pi = peers[peer]
+            if (pi["pitch"], pi["rb"], pi["q"]) != (lat.grid.pitch, lat.real_bytes, lat.q):
+                raise RuntimeError("z-neighbours disagree on the row layout")
+            if in_process:
+                tensors = table[peer]
+            else:
+                tensors = tuple(fn(*args) for fn, args in pi["handles"])
+            self.peer[face] = tensors
+            self.peer_info[face] = (pi["blocks"][facing], pi["spans"][facing])
+        self.bytes_per_exchange = sum(self.spans[f][2] for f in self.peer) * lat.real_bytes
+        ctx.barrier()   # every rank holds its peers' mappings before any phase
+
+    # -- protocol
+    def _enter_phase(self, stream):
+        self.phase += 1
+        k = self.phase
+        if self.mode == "host":
+            torch.cuda.synchronize(self.lat.device)
+            self.lat.ctx.barrier()
+            return
+        sp = _lib.stream_ptr(stream)
+        # my low face's neighbour sees me as its upper neighbour (its from_hi)
+        for face, word in ((0, 1), (1, 0)):
+            if face in self.peer:
+                flags = self.peer[face][2]
+                _lib.call("lbm_stream_signal", ctypes.c_void_p(flags.data_ptr() + 4 * word), k, sp)
+        if self.lockstep:
+            # thread ranks share one CUDA context, where a device-wide
+            # synchronisation inside torch (pinned-host allocation, cudaFree)
+            # would also wait for a peer's stream blocked on a signal this
+            # thread has not enqueued yet: enqueue every wait only after all
+            # ranks have enqueued their signal.  GPU-side ordering is still
+            # the flags' alone (the barrier does not wait for the device).
+            self.lat.ctx.barrier()
+        for face in self.peer:
+            _lib.call("lbm_stream_wait", ctypes.c_void_p(self.flags.data_ptr() + 4 * face), k, sp)
+
+    def after_collide(self, lat, stream):
+        """Phase: copy G_0's crossing runs into the neighbours' current buffer."""
+        self._enter_phase(stream)
+        mine = lat.buf[lat.cur]
+        rb = lat.real_bytes
+        for face, tensors in self.peer.items():
+            send_off, _, count = self.spans[face]
+            _, (_, recv_off, rcount) = self.peer_info[face]
+            if rcount != count:
+                raise RuntimeError("halo runs of the two sides differ")
+            _lib.call("lbm_copy_async", ctypes.c_void_p(tensors[lat.cur].data_ptr() + recv_off * rb),
+                      ctypes.c_void_p(mine.data_ptr() + send_off * rb), count * rb,
+                      _lib.stream_ptr(stream))
+
+    def boundary(self, lat, kp, src, dst, cm, tm, stream):
+        """Phase: B(n) with the crossing directions stored into the peers."""
+        self._enter_phase(stream)
+        dpar = 1 - lat.cur
+        lo = hi = None
+        if 0 in self.peer:
+            lo = ctypes.c_void_p(self.peer[0][dpar].data_ptr() + self.peer_info[0][0] * lat.real_bytes)
+        if 1 in self.peer:
+            hi = ctypes.c_void_p(self.peer[1][dpar].data_ptr() + self.peer_info[1][0] * lat.real_bytes)
+        nz = lat.box.nz
+        sp = _lib.stream_ptr(stream)
+        for z in sorted({0, nz - 1}):
+            _lib.call("lbm_fused_step_peer", lat.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
+                      z, z + 1, lo if z == 0 else None, hi if z == nz - 1 else None, sp)
+        return stream
+
+    def after_boundary(self, lat, dst, stream):
+        pass
+
+
+def select_transport(lat) -> str:
+    """'peer-device', 'peer-host', 'nccl' or 'staged' - the same on every
+    rank (decided from the environment and an all_gather of capabilities).
+    LBM_B200_HALO=nccl forces NCCL send/recv, =peer asks for the fused
+    transport also where ranks are processes sharing a GPU (host-ordered)."""
+    ctx = lat.ctx
+    want = os.environ.get("LBM_B200_HALO", "auto")
+    if want not in ("auto", "peer", "nccl"):
+        raise ValueError(f"LBM_B200_HALO must be auto, peer or nccl, got {want!r}")
+    if getattr(ctx, "backend", None) == "threads":
+        return "peer-device"
+    backend = dist.get_backend() if dist.is_initialized() else None
+    if lat.device.type != "cuda" or backend is None:
+        return "staged"
+    idx = lat.device.index if lat.device.index is not None else torch.cuda.current_device()
+    local = {str(torch.cuda.get_device_properties(i).uuid): i
+             for i in range(torch.cuda.device_count())}
+    uuid = str(torch.cuda.get_device_properties(idx).uuid)
+    caps = ctx.all_gather({"uuid": uuid, "node": os.uname().nodename})
+    shared = len({c["uuid"] for c in caps.values()}) < len(caps)
+    same_node = len({c["node"] for c in caps.values()}) == 1
+    # every peer GPU visible here and reachable by peer access (NVLink / NVSwitch)
+    can_map = same_node and all(
+        c["uuid"] in local and (local[c["uuid"]] == idx
+                                or torch.cuda.can_device_access_peer(idx, local[c["uuid"]]))
+        for c in caps.values())
+    can_map = all(ctx.all_gather(bool(can_map)).values())
+    if backend == "nccl":
+        if want == "nccl" or shared or not can_map:
+            return "nccl"
+        return "peer-device"
+    # gloo on CUDA tensors: host-staged unless the fused transport is asked for
+    if want == "peer" and same_node:
+        return "peer-host" if shared else "peer-device"
+    return "staged"
+
+
+def make_halo(lat):
+    kind = select_transport(lat)
+    if kind.startswith("peer-"):
+        return PeerHalo(lat, kind[5:])
+    return Halo(lat)

@@ -127,15 +127,98 @@ def _worker(rank, n_ranks, port, backend, device, program, args, queue):
             dist.destroy_process_group()
 
 
+class _ThreadGroup:
+    """Shared state of the ranks of one `run(..., backend="threads")`."""
+
+    def __init__(self, n_ranks: int):
+        import threading
+        self.n_ranks = n_ranks
+        self.slots = [None] * n_ranks
+        self.sync = threading.Barrier(n_ranks)
+        self.shared = {}           # rank-visible registry (the fused halo's peer table)
+
+
+class ThreadContext(Context):
+    """Rank context of one thread of an in-process rank group.
+
+    The ranks of a group are threads of one process sharing the GPU(s) it
+    sees; collectives go through a barrier and a slot per rank, in rank
+    order like the process transport.  On the device each rank keeps its own
+    streams, so the fused peer-store halo (halo.PeerHalo) runs its real
+    device-side phase protocol between the ranks' streams - without
+    processes time-sliced on one GPU, and with no kernel waiting on
+    another.  This is how the multi-rank device path is exercised on a
+    single-GPU box; production runs use one process per GPU."""
+
+    def __init__(self, group: _ThreadGroup, rank: int, device=None):
+        self.group = group
+        self.rank, self.n_ranks, self.backend = rank, group.n_ranks, "threads"
+        if device is None or device == "cuda":
+            device = torch.device("cuda", rank % max(1, torch.cuda.device_count())) \
+                if torch.cuda.is_available() else torch.device("cpu")
+        self.device = torch.device(device)
+        self.step = 0
+
+    def all_gather(self, obj) -> dict:
+        g = self.group
+        g.slots[self.rank] = pickle.dumps(obj)
+        g.sync.wait()
+        out = {r: pickle.loads(g.slots[r]) for r in range(self.n_ranks)}
+        g.sync.wait()
+        return out
+
+    def barrier(self) -> None:
+        self.group.sync.wait()
+
+
+def _run_threads(n_ranks, program, args, device, timeout):
+    import threading
+    group = _ThreadGroup(n_ranks)
+    results, errors = {}, []
+
+    def body(rank):
+        try:
+            ctx = ThreadContext(group, rank, device)
+            if ctx.device.type == "cuda":
+                # each rank its own (non-blocking) main stream, as a process
+                # would have: ranks must not serialise on the legacy stream
+                torch.cuda.set_device(ctx.device)
+                with torch.cuda.stream(torch.cuda.Stream(ctx.device)):
+                    results[rank] = program(ctx, *args)
+                    torch.cuda.current_stream(ctx.device).synchronize()
+            else:
+                results[rank] = program(ctx, *args)
+        except BaseException as exc:  # report, and release ranks blocked in a collective
+            import traceback
+            errors.append(f"rank {rank}: {type(exc).__name__}: {exc}\n{traceback.format_exc()}")
+            group.sync.abort()
+
+    threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(n_ranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout)
+        if t.is_alive():
+            raise RuntimeError(f"thread rank group did not finish within {timeout} s")
+    if errors:
+        raise RuntimeError("rank failed:\n" + "\n".join(errors))
+    return [results[r] for r in range(n_ranks)]
+
+
 def run(n_ranks: int, program, *args, backend: str = "gloo", device=None,
         timeout: float = 600.0):
     """Run `program(ctx, *args)` on `n_ranks` local processes (SimRuntime.run's
     role in the reference tests).  Returns the per-rank results in rank order.
     backend="gloo", device="cuda" runs several ranks on the GPUs present
-    (ranks may share one GPU; halos are then staged through the host)."""
+    (ranks may share one GPU; halos are then staged through the host, or go
+    through CUDA IPC peer stores with LBM_B200_HALO=peer).
+    backend="threads" runs the ranks as threads of this process
+    (ThreadContext): the fused device-side halo between the ranks' streams."""
     import torch.multiprocessing as mp
     if n_ranks == 1:
         return [program(Context(device=device if device != "cuda" else None), *args)]
+    if backend == "threads":
+        return _run_threads(n_ranks, program, args, device, timeout)
     ctxmp = mp.get_context("spawn")
     queue = ctxmp.Queue()
     port = _free_port()

@@ -426,3 +426,109 @@ def test_fp32_every_golden_case_within_1e5_relative(api, name):
         ref = gold[f"pdf_{s}"]
         rel = float(np.max(np.abs(arr - ref) / np.abs(ref)))
         assert rel < TOL_F32_REL, (name, s, rel)
+
+
+# ------------------------------------------------------------ fused halo
+_HALO_SPEC = dict(stencil="D3Q19", dims=(16, 12, 16), root_dims=(1, 1, 4),
+                  periodic=(True, True, False),
+                  geometry=dict(kind="spheres", seed=4, rmin=2.0, rmax=3.5, frac=0.2, walls_z=True),
+                  model=("TRT_magic", 1.7), force=("Guo", (1e-4, 0.0, 2e-5)), init=("random", 9),
+                  steps=12, snapshots=(1, 12), macro=True, layout="fzyx")
+
+
+@pytest.mark.parametrize("n_ranks", [2, 4])
+def test_fused_peer_halo_thread_ranks_bitwise(api, n_ranks):
+    """z-slab ranks as threads of one process, each with its own streams:
+    the boundary kernel stores the crossing directions into the neighbour's
+    ghost plane and the phases are ordered by stream flags
+    (lbm_stream_signal / lbm_stream_wait) - the device path of a multi-GPU
+    run.  Bitwise equal to 1 rank and to the oracle."""
+    import paper_1909_13772_b200 as P
+    from paper_1909_13772_b200 import halo
+    seen = []
+    orig = halo.PeerHalo.boundary
+
+    def spy(self, *a, **k):
+        seen.append(self.kind)
+        return orig(self, *a, **k)
+    halo.PeerHalo.boundary = spy
+    try:
+        multi = P.run(n_ranks, _rank_prog, _HALO_SPEC, backend="threads", device="cuda",
+                      timeout=300)[0]
+    finally:
+        halo.PeerHalo.boundary = orig
+    assert seen and set(seen) == {"peer-device"}
+    base = cases.run_case(api, _ctx(), _HALO_SPEC)
+    for s in _HALO_SPEC["snapshots"]:
+        assert multi["pdf"][s].tobytes() == base["pdf"][s].tobytes(), s
+    assert multi["macro"][0].tobytes() == base["macro"][0].tobytes()
+    assert multi["macro"][1].tobytes() == base["macro"][1].tobytes()
+    assert base["pdf"][12].tobytes() == cases.oracle_run(_HALO_SPEC, oracle)["pdf"][12].tobytes()
+
+
+def test_fused_peer_halo_periodic_z_two_thread_ranks(api):
+    """P = 2 periodic: both faces of a rank face the same peer (two flag
+    words, two ghost planes)."""
+    import paper_1909_13772_b200 as P
+    spec = dict(stencil="D3Q27", dims=(10, 8, 12), root_dims=(1, 1, 2),
+                periodic=(True, True, True), geometry=None, model=("SRT", 1.6), force=None,
+                init=("random", 1), steps=8, snapshots=(8,), layout="zyxf")
+    base = cases.run_case(api, _ctx(), spec)
+    multi = P.run(2, _rank_prog, spec, backend="threads", device="cuda", timeout=300)[0]
+    assert multi["pdf"][8].tobytes() == base["pdf"][8].tobytes()
+
+
+def test_fused_peer_halo_ipc_processes_host_ordered(api, monkeypatch):
+    """Ranks as processes sharing the GPU: peers' buffers opened from CUDA
+    IPC handles and written by the boundary kernel; phases host-ordered
+    (processes on one GPU must not wait on each other on the device)."""
+    import paper_1909_13772_b200 as P
+    monkeypatch.setenv("LBM_B200_HALO", "peer")
+    multi = P.run(2, _rank_prog, _HALO_SPEC, backend="gloo", device="cuda")[0]
+    base = cases.run_case(api, _ctx(), _HALO_SPEC)
+    for s in _HALO_SPEC["snapshots"]:
+        assert multi["pdf"][s].tobytes() == base["pdf"][s].tobytes(), s
+
+
+def test_fused_peer_halo_fp32_thread_ranks(api):
+    """fp32 storage through the fused halo == fp32 on one rank, bitwise."""
+    import paper_1909_13772_b200 as P
+    kw = {"dtype": "float32"}
+    base = cases.run_case(api, _ctx(), _HALO_SPEC, pdf_kwargs=kw)
+    multi = P.run(4, _rank_prog_kw, _HALO_SPEC, kw, backend="threads", device="cuda",
+                  timeout=300)[0]
+    for s in _HALO_SPEC["snapshots"]:
+        assert multi["pdf"][s].tobytes() == base["pdf"][s].tobytes(), s
+
+
+def _rank_prog_kw(ctx, spec, kw):
+    return cases.run_case(cases.b200_api(), ctx, spec, pdf_kwargs=kw)
+
+
+def test_stream_flag_signal_orders_a_second_stream(api):
+    """lbm_stream_signal / lbm_stream_wait: work queued behind a wait on
+    stream B runs only after stream A's earlier writes and its signal.
+    The signal is enqueued before the wait: streams of one context may share
+    a hardware queue, and a wait enqueued ahead of its own signal could then
+    block it (the fused halo enqueues every signal of a phase before any
+    wait for the same reason)."""
+    import ctypes
+    import torch
+    from paper_1909_13772_b200 import _lib
+    dev = torch.device("cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    data = torch.zeros(1 << 22, dtype=torch.float64, device=dev)
+    out = torch.empty_like(data)
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    fp = ctypes.c_void_p(flag.data_ptr())
+    with torch.cuda.stream(sa):
+        torch.cuda._sleep(2_000_000)         # keep A busy well past B's launch
+        data.fill_(3.0)
+    _lib.call("lbm_stream_signal", fp, 1, _lib.stream_ptr(sa))
+    _lib.call("lbm_stream_wait", fp, 1, _lib.stream_ptr(sb))
+    with torch.cuda.stream(sb):
+        out.copy_(data)                      # must see the fill
+    torch.cuda.synchronize()
+    assert float(out.min()) == 3.0 and float(out.max()) == 3.0
+    assert int(flag.item()) == 1

@@ -108,3 +108,49 @@ def test_host_collectives_two_ranks():
     assert res[1][1] is None
     assert res[0][2] == res[1][2] == 3.0
     assert res[0][3] == [1] and res[1][3] == [0]
+
+
+# ------------------------------------------------------ in-process rank group
+def _thread_prog(ctx, payload):
+    got = ctx.all_gather({"rank": ctx.rank, "payload": payload * (ctx.rank + 1)})
+    total = ctx.all_reduce((float(ctx.rank), 1.0), "sum")
+    ctx.barrier()
+    return got, total
+
+
+def test_thread_rank_group_collectives_in_rank_order():
+    """ThreadContext (the in-process rank group the fused device halo is
+    tested with) keeps the process transport's collective semantics."""
+    res = P.run(3, _thread_prog, 2, backend="threads", device="cpu")
+    for r, (got, total) in enumerate(res):
+        assert sorted(got) == [0, 1, 2]
+        assert [got[k]["payload"] for k in range(3)] == [2, 4, 6]
+        assert total == [3.0, 3.0]
+
+
+def _thread_fail(ctx):
+    if ctx.rank == 1:
+        raise ValueError("boom")
+    ctx.barrier()       # released by the failing rank's abort, not hung
+
+
+def test_thread_rank_group_reports_failures():
+    with pytest.raises(RuntimeError, match="boom"):
+        P.run(2, _thread_fail, backend="threads", device="cpu", timeout=60)
+
+
+def _select_prog(ctx):
+    forest = P.create_forest(ctx, (0, 0, 0, 4, 4, 2 * ctx.n_ranks), (1, 1, ctx.n_ranks),
+                             periodic=(True, True, True), cells_per_block=(4, 4, 2))
+
+    class _Lat:     # what select_transport reads of a DeviceLattice
+        pass
+    lat = _Lat()
+    lat.ctx, lat.device, lat.forest = ctx, torch.device("cpu"), forest
+    return halo.select_transport(lat)
+
+
+def test_transport_selection_on_cpu_ranks():
+    # CPU tensors over gloo: the host-staged transport; threads: the fused one
+    assert P.run(2, _select_prog, backend="gloo") == ["staged", "staged"]
+    assert P.run(2, _select_prog, backend="threads", device="cpu") == ["peer-device"] * 2
