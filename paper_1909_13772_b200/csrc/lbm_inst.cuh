@@ -29,15 +29,27 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
     if (z1 <= z0) return cudaSuccess;
     dim3 b = fused_block(g.nx);
     dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
+    const bool peer = p.peer_lo != nullptr || p.peer_hi != nullptr;
     if (p.mv_link) {
         // moving-body walls: a separate instantiation, so the standard sweep
         // keeps its register allocation (3D stencils, SRT/TRT/dense MRT)
         if constexpr (Q != 9 && MODEL <= 2 && FORCE != 2) {
-            k_fused<Q, LBM_REAL, MODEL, FORCE, true><<<grid, b, 0, s>>>(
-                g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0);
+            if (peer)
+                k_fused<Q, LBM_REAL, MODEL, FORCE, true, true><<<grid, b, 0, s>>>(
+                    g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0);
+            else
+                k_fused<Q, LBM_REAL, MODEL, FORCE, true><<<grid, b, 0, s>>>(
+                    g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0);
             return cudaGetLastError();
         } else {
             return cudaErrorInvalidValue;
+        }
+    }
+    if constexpr (Q != 9) {
+        if (peer) {
+            k_fused<Q, LBM_REAL, MODEL, FORCE, false, true><<<grid, b, 0, s>>>(
+                g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0);
+            return cudaGetLastError();
         }
     }
     k_fused<Q, LBM_REAL, MODEL, FORCE><<<grid, b, 0, s>>>(g, p, (const LBM_REAL*)src,

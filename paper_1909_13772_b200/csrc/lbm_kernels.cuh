@@ -393,7 +393,13 @@ constexpr int fused_minb_bx() {
     return m < 1 ? 1 : m;
 }
 
-template <int Q, typename Real, int MODEL, int FORCE, bool MOVING = false>
+// PEER: the launch carries the fused z-face halo (KParams::peer_lo / peer_hi,
+// boundary planes of a multi-rank step only); a separate instantiation so
+// the interior / single-rank kernels keep their register allocation.
+// (Measured and rejected: visiting rows in tiles of 8..64 rows, all planes of
+// a tile first, to bring the z-neighbour that re-reads a bounce-back source
+// closer in time: -1..-8 % on configs 4 fp64 / fp32 and 2.)
+template <int Q, typename Real, int MODEL, int FORCE, bool MOVING = false, bool PEER = false>
 __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
     k_fused(KGrid g, KParams p, const Real* __restrict__ src,
                                                Real* __restrict__ dst,
@@ -403,7 +409,6 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y;
     const int z = z0 + blockIdx.z;
-    // warp-uniform choice of the index path: wrapping only near periodic edges
     const int xw0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     const bool edge_x = g.wrap_x && (xw0 == 0 || xw0 + 32 >= g.nx);
     const bool edge_y = g.wrap_y && (y == 0 || y == g.ny - 1);
@@ -426,6 +431,7 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
     // HBM over NVLink, or another slab on this device) - the per-step
     // exchange of field/ghost.py:202-264 without a separate send/recv.
     // Block-uniform (z is per block), so interior planes pay one test.
+    if constexpr (PEER) {
     if (z == 0 && p.peer_lo != nullptr) {
         Real* pp = opaque(static_cast<Real*>(p.peer_lo) + (int64_t)(y + 1) * g.pitch + g.xoff + x);
         static_for<0, Q>([&](auto I_) {
@@ -439,6 +445,7 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
             constexpr int i = decltype(I_)::value;
             if constexpr (D::cz[i] == 1) store_any<Q, i>(pp + g.dslot[i], f[i]);
         });
+    }
     }
 }
 
