@@ -3,8 +3,12 @@
 // lbm_inst_f32.cu (REAL=float storage, fp64 registers, FMA allowed).
 #pragma once
 #include <stdlib.h>
+#include <string.h>
 #include "lbm_kernels.cuh"
 #include "lbm_launch.h"
+#ifdef LBM_TMA_VARIANT
+#include "lbm_tma.cuh"
+#endif
 
 #ifndef LBM_REAL
 #error "define LBM_REAL before including lbm_inst.cuh"
@@ -23,10 +27,118 @@ inline dim3 fused_block(int nx) {
     return dim3(bx, 1, 1);
 }
 
+#ifdef LBM_TMA_VARIANT
+// ---------------------------------------------------------------- TMA path
+// Built only into variant libraries (-DLBM_TMA_VARIANT, see lbm_tma.cuh for
+// the design and the B200 measurements that keep it out of the default
+// build).  In such a build LBM_B200_FUSED=ldg selects the LDG kernel.
+inline bool use_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("LBM_B200_FUSED");
+        v = (e && strcmp(e, "ldg") == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
+typedef CUresult (*pfn_tmap_encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                      CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// The field as a 3-D tensor (x: pitch, y: ny+2 rows, q*(nz+2) z-slot planes),
+// box = one 128-cell row segment.  Encoded once per (buffer, geometry).
+inline int tma_box_width(const KGrid& g) {
+    constexpr int a = tma_margin<LBM_REAL>();   // 16 bytes of cells
+    return (g.nx >= kTmaW ? kTmaW : (g.nx + a - 1) / a * a) + 2 * a;
+}
+
+inline cudaError_t field_tmap(CUtensorMap* out, const void* base, const KGrid& g, int q) {
+    static pfn_tmap_encode_t enc = nullptr;
+    if (!enc) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) !=
+                cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess || !fn)
+            return cudaErrorNotSupported;
+        enc = (pfn_tmap_encode_t)fn;
+    }
+    struct Entry {
+        const void* base;
+        int nx, ny, nz, pitch, q;
+        CUtensorMap map;
+    };
+    static thread_local Entry cache[4];
+    static thread_local int next = 0;
+    for (auto& e : cache)
+        if (e.base == base && e.nx == g.nx && e.ny == g.ny && e.nz == g.nz && e.pitch == g.pitch &&
+            e.q == q) {
+            *out = e.map;
+            return cudaSuccess;
+        }
+    const cuuint64_t dims[3] = {(cuuint64_t)g.pitch, (cuuint64_t)(g.ny + 2),
+                                (cuuint64_t)q * (g.nz + 2)};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * sizeof(LBM_REAL),
+                                   (cuuint64_t)g.plane * sizeof(LBM_REAL)};
+    const cuuint32_t box[3] = {(cuuint32_t)tma_box_width(g), 1, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(out,
+                     sizeof(LBM_REAL) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    Entry& e = cache[next];
+    next = (next + 1) % 4;
+    e = Entry{base, g.nx, g.ny, g.nz, g.pitch, q, *out};
+    return cudaSuccess;
+}
+
+template <int Q, int MODEL, int FORCE>
+cudaError_t fused_tma_t(const KGrid& g, const KParams& p, const void* src, void* dst,
+                        const uint32_t* cm, const uint32_t* tmk, int z0, int z1, cudaStream_t s) {
+    auto kern = k_fused_tma<Q, LBM_REAL, MODEL, FORCE>;
+    constexpr int smem = tma_smem_bytes<Q, LBM_REAL>();
+    static int ctas = 0;   // persistent grid: SMs x resident CTAs
+    if (ctas == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        int occ = 0, dev = 0, sms = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTmaThreads, smem)) !=
+            cudaSuccess)
+            return e;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        ctas = sms * (occ > 0 ? occ : 1);
+    }
+    CUtensorMap map;
+    cudaError_t e = field_tmap(&map, src, g, Q);
+    if (e != cudaSuccess) return e;
+    const int nxt = (g.nx + kTmaW - 1) / kTmaW;
+    const int64_t ntiles = (int64_t)nxt * g.ny * (z1 - z0);
+    if (ntiles >= (int64_t)1 << 31) return cudaErrorInvalidValue;   // 32-bit tile indices
+    const int grid = (int)(ntiles < ctas ? ntiles : ctas);
+    kern<<<grid, kTmaThreads, smem, s>>>(map, g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0,
+                                         nxt, ntiles, tma_box_width(g));
+    return cudaGetLastError();
+}
+
+#endif  // LBM_TMA_VARIANT
+
 template <int Q, int MODEL, int FORCE>
 cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst,
                     const uint32_t* cm, const uint32_t* tmk, int z0, int z1, cudaStream_t s) {
     if (z1 <= z0) return cudaSuccess;
+    // TMA staging for the 3-D SRT / TRT / factorised-MRT sweeps (the dense
+    // MRT tables and SimpleShift keep the LDG kernel)
+#ifdef LBM_TMA_VARIANT
+    if constexpr (Q != 9 && MODEL != 2 && FORCE != 2) {
+        if (!p.mv_link && !p.peer_lo && !p.peer_hi && use_tma())
+            return fused_tma_t<Q, MODEL, FORCE>(g, p, src, dst, cm, tmk, z0, z1, s);
+    }
+#endif
     dim3 b = fused_block(g.nx);
     dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
     const bool peer = p.peer_lo != nullptr || p.peer_hi != nullptr;

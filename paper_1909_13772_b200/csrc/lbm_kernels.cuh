@@ -224,6 +224,12 @@ __device__ __forceinline__ void moving_links(const KGrid& g, const KParams& p, i
     }
 }
 
+template <int Q, typename Real, typename Acc, int MV>
+__device__ __forceinline__ void pull_finish(const KGrid& g, const KParams& p,
+                                            const Real* __restrict__ src, int x, int y, int z,
+                                            int64_t own, uint32_t code, uint2 t, const Real (&raw)[Q],
+                                            Acc (&f)[Q]);
+
 // Load the 19/27/9 pulled populations of cell (x,y,z) with the fused
 // bounce-back substitution R[x,i] = G[x,opp(i)] (- UBB term) for masked
 // directions (boundary.py:163-170).
@@ -276,8 +282,6 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                   "fp32 registers only for fp32 storage");
     using D = Dirs<Q>;
     const int64_t own = lidx(g, z, 0, y, x);
-    constexpr uint32_t kTyped = LBM_MASK_UBB | LBM_MASK_PRESSURE | (MV ? LBM_MASK_MOVING : 0u);
-    const bool typed = (code & kTyped) != 0u;
     uint2 t = make_uint2(0u, 0u);
     if (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) t = __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
     Real raw[Q];
@@ -305,6 +309,19 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
             raw[i] = __ldg(src + off[i]);
         });
     }
+    pull_finish<Q, Real, Acc, MV>(g, p, src, x, y, z, own, code, t, raw, f);
+}
+
+// Phase 3 of a pull: widen the raw pulled values and apply the rare UBB /
+// Pressure / moving-wall corrections (shared by the LDG and TMA kernels).
+template <int Q, typename Real, typename Acc, int MV>
+__device__ __forceinline__ void pull_finish(const KGrid& g, const KParams& p,
+                                            const Real* __restrict__ src, int x, int y, int z,
+                                            int64_t own, uint32_t code, uint2 t, const Real (&raw)[Q],
+                                            Acc (&f)[Q]) {
+    using D = Dirs<Q>;
+    constexpr uint32_t kTyped = LBM_MASK_UBB | LBM_MASK_PRESSURE | (MV ? LBM_MASK_MOVING : 0u);
+    const bool typed = (code & kTyped) != 0u;
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
         if constexpr (std::is_same_v<Acc, double>) f[i] = Store<Real>::template widen<Q, i>(raw[i]);

@@ -5,8 +5,13 @@ tail -1 gpurun_out/pytest_gpu.log
 for cfg in ${CFGS:-"--config c4" "--config c4 --dtype f32" "--config c2"}; do
  for rep in ${REPS:-1}; do
   for v in ${VARIANTS:-default}; do
-    if [ "$v" = default ]; then unset LBM_B200_LIB; else export LBM_B200_LIB=$PWD/paper_1909_13772_b200/_lbm_b200_$v.so; fi
-    tag=$(echo "$cfg" | tr -d ' -')_$v
+    unset LBM_B200_LIB LBM_B200_FUSED
+    case "$v" in
+      default) ;;
+      fused=*) export LBM_B200_FUSED=${v#fused=} ;;
+      *) export LBM_B200_LIB=$PWD/paper_1909_13772_b200/_lbm_b200_$v.so ;;
+    esac
+    tag=$(echo "$cfg" | tr -d ' -')_$(echo $v | tr -d '=')
     timeout 600 python bench.py --steps ${STEPS:-40} --warmup 5 --no-e2e --no-cpu-baseline $cfg > gpurun_out/ab_$tag.log 2>&1
     echo "$cfg" v=$v $(python -c "import json;d=json.loads(open('gpurun_out/ab_$tag.log').read().strip().splitlines()[-1]);print(d['value'], d['roofline']['frac'], d['ms_per_step'], d['clocks']['sm_mhz'], d['clocks']['reasons'])" 2>&1 | tail -1)
   done
