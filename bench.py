@@ -360,6 +360,7 @@ def main():
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": cfg["desc"], "global_cells": [dims[0], dims[1], dims[2] * n],
                        "cells_per_gpu": cells_rank, "parallelism": f"z-slab x{n}",
+                       "halo": (getattr(lat._halo, "kind", None) if n > 1 else None),
                        "pdf_storage": "fp64" if rb == 8 else "fp32 (f - w_i), fp64 arithmetic",
                        "l2": f"working set {2 * lat.elems * rb / 1e9:.1f} GB per GPU >> 126 MB L2 "
                              "(no flush needed)"},

@@ -294,7 +294,13 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
         static_for<0, Q>([&](auto I_) {
             constexpr int i = decltype(I_)::value;
             int d = g.dpull[i];
-            if constexpr (i > 0) d = ((code >> i) & 1u) ? g.dlink[i] : d;
+            // link source = own cell, slot opp(i): the store delta of opp(i)
+            // (KGrid::dlink[i] == dslot[opp(i)]), so the select reuses the
+            // constant the store phase loads anyway
+            if constexpr (i > 0) {
+                constexpr int k = D::opp[i];
+                d = ((code >> i) & 1u) ? g.dslot[k] : d;
+            }
             raw[i] = __ldg(sp + d);
         });
     } else {
@@ -392,6 +398,9 @@ __device__ __forceinline__ void collide_any(Acc (&f)[Q], const KParams& p, int64
     else collide_cell_c32<Q, MODEL, FORCE>(f, p, om);
 }
 
+// (Measured on B200 and dropped: st.global.cs and an L2 evict_first policy on
+// these stores, to keep re-read lines in L2 - within noise on configs 4 / 2,
+// -1.3 % in fp32.)
 template <int Q, int I, typename Real, typename Acc>
 __device__ __forceinline__ void store_any(Real* p, Acc v) {
     if constexpr (std::is_same_v<Acc, double>) Store<Real>::template store<Q, I>(p, v);

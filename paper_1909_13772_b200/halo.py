@@ -220,6 +220,47 @@ class PeerHalo:
             self.peer_info[face] = (pi["blocks"][facing], pi["spans"][facing])
         self.bytes_per_exchange = sum(self.spans[f][2] for f in self.peer) * lat.real_bytes
         ctx.barrier()   # every rank holds its peers' mappings before any phase
+        if mode == "device":
+            self._handshake()
+
+    def _handshake(self, timeout_s: float = 30.0):
+        """Setup-time check of the device signalling path, without any
+        device-side wait: every rank writes a token into its neighbours'
+        flag words with the same stream memory op the phases use, then the
+        host polls its own words.  Raises PeerHaloUnavailable (the caller
+        falls back to send/recv on every rank) if a token does not arrive -
+        e.g. memory ops on peer mappings unsupported - so a broken path
+        fails at setup instead of hanging a sweep."""
+        import time
+        lat, ctx = self.lat, self.lat.ctx
+        token = 0x5A5A0001
+        sp = _lib.stream_ptr(torch.cuda.current_stream(lat.device))
+        ok = True
+        try:
+            for face, word in ((0, 1), (1, 0)):
+                if face in self.peer:
+                    flags = self.peer[face][2]
+                    _lib.call("lbm_stream_signal", ctypes.c_void_p(flags.data_ptr() + 4 * word),
+                              token, sp)
+            torch.cuda.current_stream(lat.device).synchronize()
+            t0 = time.monotonic()
+            while True:
+                got = self.flags.cpu().tolist()
+                if all(got[f] == token for f in self.peer):
+                    break
+                if time.monotonic() - t0 > timeout_s:
+                    ok = False
+                    break
+                time.sleep(0.001)
+        except Exception:
+            ok = False
+        ok = all(ctx.all_gather(ok).values())
+        # nobody writes the words any more: reset them for phase 1
+        self.flags.zero_()
+        torch.cuda.current_stream(lat.device).synchronize()
+        ctx.barrier()
+        if not ok:
+            raise PeerHaloUnavailable("stream memory ops on peer mappings did not arrive")
 
     # -- protocol
     def _enter_phase(self, stream):
@@ -317,8 +358,16 @@ def select_transport(lat) -> str:
     return "staged"
 
 
+class PeerHaloUnavailable(RuntimeError):
+    """The fused halo's setup check failed on some rank (collective)."""
+
+
 def make_halo(lat):
     kind = select_transport(lat)
     if kind.startswith("peer-"):
-        return PeerHalo(lat, kind[5:])
+        try:
+            return PeerHalo(lat, kind[5:])
+        except PeerHaloUnavailable as exc:
+            import warnings
+            warnings.warn(f"fused peer halo unavailable ({exc}); using send/recv", RuntimeWarning)
     return Halo(lat)
