@@ -9,6 +9,9 @@
 #ifdef LBM_TMA_VARIANT
 #include "lbm_tma.cuh"
 #endif
+#ifdef LBM_VEC_VARIANT
+#include "lbm_vec.cuh"
+#endif
 
 #ifndef LBM_REAL
 #error "define LBM_REAL before including lbm_inst.cuh"
@@ -127,12 +130,48 @@ cudaError_t fused_tma_t(const KGrid& g, const KParams& p, const void* src, void*
 
 #endif  // LBM_TMA_VARIANT
 
+#ifdef LBM_VEC_VARIANT
+// ------------------------------------------------------- vectorised path
+// Variant builds only (-DLBM_VEC_VARIANT; lbm_vec.cuh has the B200
+// measurements).  LBM_B200_VEC=0|1 overrides the build default at run time.
+#ifndef LBM_VEC_DEFAULT
+#define LBM_VEC_DEFAULT 1
+#endif
+inline bool use_vec() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("LBM_B200_VEC");
+        v = e ? (atoi(e) != 0) : LBM_VEC_DEFAULT;
+    }
+    return v == 1;
+}
+
+template <int Q, int MODEL, int FORCE>
+cudaError_t fused_vec_t(const KGrid& g, const KParams& p, const void* src, void* dst,
+                        const uint32_t* cm, const uint32_t* tmk, int z0, int z1, cudaStream_t s) {
+    constexpr int V = std::is_same_v<LBM_REAL, double> ? 2 : LBM_VEC_WIDTH;
+    const int groups = g.nx / V;
+    const int bx = groups >= 128 ? 128 : ((groups + 31) / 32) * 32;
+    dim3 grid((groups + bx - 1) / bx, g.ny, z1 - z0);
+    k_fused_vec<Q, LBM_REAL, MODEL, FORCE, V><<<grid, bx, 0, s>>>(
+        g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0);
+    return cudaGetLastError();
+}
+#endif  // LBM_VEC_VARIANT
+
 template <int Q, int MODEL, int FORCE>
 cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst,
                     const uint32_t* cm, const uint32_t* tmk, int z0, int z1, cudaStream_t s) {
     if (z1 <= z0) return cudaSuccess;
     // TMA staging for the 3-D SRT / TRT / factorised-MRT sweeps (the dense
     // MRT tables and SimpleShift keep the LDG kernel)
+#ifdef LBM_VEC_VARIANT
+    if constexpr (Q != 9 && MODEL != 2 && FORCE != 2) {
+        constexpr int V = std::is_same_v<LBM_REAL, double> ? 2 : LBM_VEC_WIDTH;
+        if (!p.mv_link && !p.peer_lo && !p.peer_hi && g.nx % V == 0 && use_vec())
+            return fused_vec_t<Q, MODEL, FORCE>(g, p, src, dst, cm, tmk, z0, z1, s);
+    }
+#endif
 #ifdef LBM_TMA_VARIANT
     if constexpr (Q != 9 && MODEL != 2 && FORCE != 2) {
         if (!p.mv_link && !p.peer_lo && !p.peer_hi && use_tma())

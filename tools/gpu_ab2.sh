@@ -5,10 +5,12 @@ tail -1 gpurun_out/pytest_gpu.log
 for cfg in ${CFGS:-"--config c4" "--config c4 --dtype f32" "--config c2"}; do
  for rep in ${REPS:-1}; do
   for v in ${VARIANTS:-default}; do
-    unset LBM_B200_LIB LBM_B200_FUSED
+    unset LBM_B200_LIB LBM_B200_FUSED LBM_B200_VEC
     case "$v" in
       default) ;;
       fused=*) export LBM_B200_FUSED=${v#fused=} ;;
+      vec=*) export LBM_B200_VEC=${v#vec=} ;;
+      vec+*) export LBM_B200_VEC=1 LBM_B200_LIB=$PWD/paper_1909_13772_b200/_lbm_b200_${v#vec+}.so ;;
       *) export LBM_B200_LIB=$PWD/paper_1909_13772_b200/_lbm_b200_$v.so ;;
     esac
     tag=$(echo "$cfg" | tr -d ' -')_$(echo $v | tr -d '=')
