@@ -222,6 +222,16 @@ int lbm_stream_signal(void* flag, uint32_t value, void* stream);
  * a peer GPU's mapped HBM): the fused halo's full-run copy after
  * lbm_collide_only. */
 int lbm_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* CUDA IPC of the fused halo's buffers (ABI 4).  export: 64-byte
+ * cudaIpcMemHandle_t of the allocation holding `ptr` plus the byte offset of
+ * `ptr` in it (buffers may be sub-allocated by a caching allocator).  open:
+ * map a peer's handle into the CURRENT device (lazy peer access: the
+ * neighbour may be another GPU of the node); the caller adds the offset.
+ * close: unmap a base returned by open. */
+int lbm_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
+int lbm_ipc_open(const void* handle, void** base_out);
+int lbm_ipc_close(void* base);
 int lbm_stream_wait(const void* flag, uint32_t value, void* stream);
 
 /* Collide, in place, every interior cell whose cellmask has LBM_MASK_FLUID

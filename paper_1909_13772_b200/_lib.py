@@ -30,6 +30,7 @@ EXPORTS = (
     "lbm_collide_cells", "lbm_equilibrium_cells", "lbm_macroscopic_cells",
     "lbm_build_moving_masks", "lbm_fused_step_peer", "lbm_ghost_block_offset",
     "lbm_stream_signal", "lbm_stream_wait", "lbm_copy_async",
+    "lbm_ipc_export", "lbm_ipc_open", "lbm_ipc_close",
 )
 
 
@@ -104,6 +105,9 @@ def load(path: Path | None = None):
         "lbm_stream_signal": ([P, ctypes.c_uint32, P], I),
         "lbm_stream_wait": ([P, ctypes.c_uint32, P], I),
         "lbm_copy_async": ([P, P, I64, P], I),
+        "lbm_ipc_export": ([P, P, ctypes.POINTER(I64)], I),
+        "lbm_ipc_open": ([P, ctypes.POINTER(P)], I),
+        "lbm_ipc_close": ([P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -515,6 +515,55 @@ int memops_init() {
 }
 }  // namespace
 
+// CUDA IPC for the fused halo: export a (possibly sub-allocated) device
+// buffer as handle + offset from its allocation base, and open a peer's
+// export in the CURRENT device's context with lazy peer access, so a
+// kernel on this GPU can store into a neighbour GPU's HBM over NVLink
+// without a second context on the neighbour's device.
+namespace {
+typedef CUresult (*pfn_range_t)(CUdeviceptr*, size_t*, CUdeviceptr);
+}  // namespace
+
+int lbm_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) {
+    if (!ptr || !handle_out || !offset_out) return fail(LBM_EINVAL, "NULL argument");
+    static pfn_range_t range = nullptr;
+    if (!range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(LBM_ECUDA, "driver entry point cuMemGetAddressRange unavailable");
+        range = (pfn_range_t)fn;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+        return fail(LBM_EINVAL, "pointer is not device memory");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcGetMemHandle");
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)((CUdeviceptr)ptr - base);
+    return LBM_OK;
+}
+
+int lbm_ipc_open(const void* handle, void** base_out) {
+    if (!handle || !base_out) return fail(LBM_EINVAL, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcOpenMemHandle");
+    *base_out = base;
+    return LBM_OK;
+}
+
+int lbm_ipc_close(void* base) {
+    if (!base) return LBM_OK;
+    return cuda_status(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
+}
+
 int lbm_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
     if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(LBM_EINVAL, "bad copy");
     if (bytes == 0) return LBM_OK;

@@ -141,6 +141,14 @@ class Halo:
 
 
 # ------------------------------------------------------------ fused halo
+def _ipc_export(t):
+    """(64-byte IPC handle, byte offset) of a device tensor's storage."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _lib.call("lbm_ipc_export", ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off))
+    return h.raw, off.value
+
+
 def _face_geometry(lat):
     """(send_off, count) per face and the receiving ghost-block offsets."""
     spans = face_spans(lat.gref)
@@ -176,8 +184,9 @@ class PeerHalo:
     GPU; the phase entry is a device synchronize + a host barrier instead of
     stream waits, because processes time-sliced on one GPU must not wait on
     each other on the device (B200_PROFILING: Xid 109).  Peers in another
-    process are opened from CUDA IPC handles (torch.multiprocessing's
-    reduction); in-process peers are used directly."""
+    process are mapped from CUDA IPC handles into this GPU's context with
+    lazy peer access (lbm_ipc_export / lbm_ipc_open); in-process peers are
+    used directly.  self.peer holds raw device addresses."""
 
     def __init__(self, lat, mode: str):
         self.kind = "peer-" + mode
@@ -195,15 +204,15 @@ class PeerHalo:
         if in_process:
             key = ("peer-halo", id(lat.forest.ctx.group), lat.pdf.key)
             table = ctx.group.shared.setdefault(key, {})
-            table[ctx.rank] = (lat.buf[0], lat.buf[1], self.flags)
+            table[ctx.rank] = tuple(t.data_ptr() for t in (lat.buf[0], lat.buf[1], self.flags))
             mine = None
         else:
-            from torch.multiprocessing.reductions import reduce_tensor
-            mine = tuple(reduce_tensor(t) for t in (lat.buf[0], lat.buf[1], self.flags))
+            mine = tuple(_ipc_export(t) for t in (lat.buf[0], lat.buf[1], self.flags))
+        self._opened = {}       # handle bytes -> mapped base (closed in close())
         info = {"handles": mine, "spans": self.spans, "blocks": self.blocks,
                 "pitch": lat.grid.pitch, "rb": lat.real_bytes, "q": lat.q}
         peers = ctx.all_gather(info)
-        self.peer = {}          # face -> (buf0, buf1, flags) of the neighbour across it
+        self.peer = {}          # face -> addresses (buf0, buf1, flags) of the neighbour across it
         self.peer_info = {}
         for face, peer, facing in ((0, box.lo_peer, 1), (1, box.hi_peer, 0)):
             zmode = box.zface_lo if face == 0 else box.zface_hi
@@ -213,10 +222,10 @@ class PeerHalo:
             if (pi["pitch"], pi["rb"], pi["q"]) != (lat.grid.pitch, lat.real_bytes, lat.q):
                 raise RuntimeError("z-neighbours disagree on the row layout")
             if in_process:
-                tensors = table[peer]
+                addrs = table[peer]
             else:
-                tensors = tuple(fn(*args) for fn, args in pi["handles"])
-            self.peer[face] = tensors
+                addrs = tuple(self._open(h, off) for h, off in pi["handles"])
+            self.peer[face] = addrs
             self.peer_info[face] = (pi["blocks"][facing], pi["spans"][facing])
         self.bytes_per_exchange = sum(self.spans[f][2] for f in self.peer) * lat.real_bytes
         ctx.barrier()   # every rank holds its peers' mappings before any phase
@@ -240,8 +249,7 @@ class PeerHalo:
             for face, word in ((0, 1), (1, 0)):
                 if face in self.peer:
                     flags = self.peer[face][2]
-                    _lib.call("lbm_stream_signal", ctypes.c_void_p(flags.data_ptr() + 4 * word),
-                              token, sp)
+                    _lib.call("lbm_stream_signal", ctypes.c_void_p(flags + 4 * word), token, sp)
             torch.cuda.current_stream(lat.device).synchronize()
             t0 = time.monotonic()
             while True:
@@ -262,6 +270,23 @@ class PeerHalo:
         if not ok:
             raise PeerHaloUnavailable("stream memory ops on peer mappings did not arrive")
 
+    def _open(self, handle: bytes, offset: int) -> int:
+        """Map a peer allocation once per handle (P = 2 periodic: both faces
+        face the same rank) and return the address of its buffer."""
+        base = self._opened.get(handle)
+        if base is None:
+            out = ctypes.c_void_p()
+            _lib.call("lbm_ipc_open", handle, ctypes.byref(out))
+            base = self._opened[handle] = out.value
+        return base + offset
+
+    def close(self):
+        """Unmap the neighbours' buffers (collective: nobody may still write)."""
+        opened, self._opened = getattr(self, "_opened", {}), {}
+        for base in opened.values():
+            _lib.call("lbm_ipc_close", ctypes.c_void_p(base))
+        self.peer = {}
+
     # -- protocol
     def _enter_phase(self, stream):
         self.phase += 1
@@ -275,7 +300,7 @@ class PeerHalo:
         for face, word in ((0, 1), (1, 0)):
             if face in self.peer:
                 flags = self.peer[face][2]
-                _lib.call("lbm_stream_signal", ctypes.c_void_p(flags.data_ptr() + 4 * word), k, sp)
+                _lib.call("lbm_stream_signal", ctypes.c_void_p(flags + 4 * word), k, sp)
         if self.lockstep:
             # thread ranks share one CUDA context, where a device-wide
             # synchronisation inside torch (pinned-host allocation, cudaFree)
@@ -292,12 +317,12 @@ class PeerHalo:
         self._enter_phase(stream)
         mine = lat.buf[lat.cur]
         rb = lat.real_bytes
-        for face, tensors in self.peer.items():
+        for face, addrs in self.peer.items():
             send_off, _, count = self.spans[face]
             _, (_, recv_off, rcount) = self.peer_info[face]
             if rcount != count:
                 raise RuntimeError("halo runs of the two sides differ")
-            _lib.call("lbm_copy_async", ctypes.c_void_p(tensors[lat.cur].data_ptr() + recv_off * rb),
+            _lib.call("lbm_copy_async", ctypes.c_void_p(addrs[lat.cur] + recv_off * rb),
                       ctypes.c_void_p(mine.data_ptr() + send_off * rb), count * rb,
                       _lib.stream_ptr(stream))
 
@@ -307,9 +332,9 @@ class PeerHalo:
         dpar = 1 - lat.cur
         lo = hi = None
         if 0 in self.peer:
-            lo = ctypes.c_void_p(self.peer[0][dpar].data_ptr() + self.peer_info[0][0] * lat.real_bytes)
+            lo = ctypes.c_void_p(self.peer[0][dpar] + self.peer_info[0][0] * lat.real_bytes)
         if 1 in self.peer:
-            hi = ctypes.c_void_p(self.peer[1][dpar].data_ptr() + self.peer_info[1][0] * lat.real_bytes)
+            hi = ctypes.c_void_p(self.peer[1][dpar] + self.peer_info[1][0] * lat.real_bytes)
         nz = lat.box.nz
         sp = _lib.stream_ptr(stream)
         for z in sorted({0, nz - 1}):
