@@ -187,7 +187,9 @@ int lbm_face_span(const lbm_grid_t* g, int face, int64_t* send_off,
  * ghosts valid), bounce-back on masked links, collide fluid cells, store
  * G_{n+1} into dst.  cellmask: (nz, ny, nx) uint32 from lbm_build_cellmask;
  * typemask: (nz, ny, nx, 2) uint32 - word 0 UBB link bits, word 1 Pressure
- * link bits - only read where LBM_MASK_UBB / LBM_MASK_PRESSURE is set. */
+ * link bits - only read where LBM_MASK_UBB / LBM_MASK_PRESSURE is set.
+ * cellmask = typemask = NULL: every cell is fluid and has no link (a
+ * periodic domain without boundary handling); no mask bytes are read. */
 int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p,
                    const void* src, void* dst, const uint32_t* cellmask,
                    const uint32_t* typemask, int z_begin, int z_end,

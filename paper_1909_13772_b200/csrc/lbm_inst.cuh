@@ -168,13 +168,13 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
 #ifdef LBM_VEC_VARIANT
     if constexpr (Q != 9 && MODEL != 2 && FORCE != 2) {
         constexpr int V = std::is_same_v<LBM_REAL, double> ? 2 : LBM_VEC_WIDTH;
-        if (!p.mv_link && !p.peer_lo && !p.peer_hi && g.nx % V == 0 && use_vec())
+        if (!p.mv_link && !p.peer_lo && !p.peer_hi && cm && g.nx % V == 0 && use_vec())
             return fused_vec_t<Q, MODEL, FORCE>(g, p, src, dst, cm, tmk, z0, z1, s);
     }
 #endif
 #ifdef LBM_TMA_VARIANT
     if constexpr (Q != 9 && MODEL != 2 && FORCE != 2) {
-        if (!p.mv_link && !p.peer_lo && !p.peer_hi && use_tma())
+        if (!p.mv_link && !p.peer_lo && !p.peer_hi && cm && use_tma())
             return fused_tma_t<Q, MODEL, FORCE>(g, p, src, dst, cm, tmk, z0, z1, s);
     }
 #endif

@@ -442,7 +442,9 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
     const bool generic = edge_x || edge_y || edge_z;
     if (x >= g.nx) return;
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
-    const uint32_t code = __ldg(cellmask + cell);
+    // cellmask == NULL: every cell fluid, no links (periodic runs without a
+    // boundary handling) - saves the 4 B/cell mask read
+    const uint32_t code = cellmask ? __ldg(cellmask + cell) : LBM_MASK_FLUID;
     using Acc = AccOf<Real>;
     Acc f[Q];
     pull_cell<Q, Real, Acc, MOVING ? 2 : 0>(g, p, src, x, y, z, code, typemask, generic, f);

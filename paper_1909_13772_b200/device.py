@@ -126,17 +126,18 @@ class RankBox:
 class Masks:
     """Device cell mask + link-type mask for one (box, stencil, flags) state."""
 
-    def __init__(self, cellmask, typemask, counts, unflagged_cell=None):
+    def __init__(self, cellmask, typemask, counts, unflagged_cell=None, all_fluid=False):
         self.cellmask = cellmask      # int32 (nz, ny, nx)
         self.typemask = typemask      # int32 (nz, ny, nx, 2)
         self.counts = counts          # dict NoSlip/UBB/Pressure -> links on this rank
         self.unflagged_cell = unflagged_cell
+        self.all_fluid = all_fluid    # the fused step may skip the mask (NULL)
 
 
 def all_fluid_masks(box: RankBox, device) -> Masks:
     cm = torch.full((box.nz, box.ny, box.nx), _lib.MASK_FLUID, dtype=torch.int32, device=device)
     tm = torch.zeros((box.nz, box.ny, box.nx, 2), dtype=torch.int32, device=device)
-    return Masks(cm, tm, {"NoSlip": 0, "UBB": 0, "Pressure": 0})
+    return Masks(cm, tm, {"NoSlip": 0, "UBB": 0, "Pressure": 0}, all_fluid=True)
 
 
 class DeviceLattice:
@@ -427,7 +428,10 @@ class DeviceLattice:
         """nsteps fused sweeps G_{n+1} = C(S(G_n))."""
         self.ensure_collided(kp, key, masks)
         nz = self.box.nz
-        cm, tm = _lib.ptr(masks.cellmask), _lib.ptr(masks.typemask)
+        if masks.all_fluid:
+            cm = tm = None      # fused step reads no mask bytes
+        else:
+            cm, tm = _lib.ptr(masks.cellmask), _lib.ptr(masks.typemask)
         lib = _lib.load()
         main = self.stream
         if self.has_halo:
