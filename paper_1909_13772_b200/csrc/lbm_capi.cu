@@ -74,6 +74,10 @@ int check_grid(const lbm_grid_t* g, KGrid* k) {
                     (long long)k->plane);
     k->plane32 = (int)k->plane;
     k->zstride32 = (int)k->zstride;
+    // keep-in-L2 hints for the bounce-back re-reads only where a z-plane of
+    // the field is large against L2 (measured: +1.9 % on config 4 at 512^2,
+    // -1.2 % on config 1 at 128^2 where the re-reads hit anyway)
+    k->link_hint = k->zstride * g->real_bytes >= ((int64_t)16 << 20) ? 1 : 0;
     auto fill = [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         using D = Dirs<Q>;

@@ -33,6 +33,7 @@ struct KGrid {
     int64_t plane;                 // (ny+2) * pitch
     int64_t zstride;               // q * plane
     int plane32, zstride32;        // the same as int (the C-ABI checks (q+2) plane < 2^31)
+    int link_hint;                 // 1: z-planes large against L2 (see ldg_keep)
     // own-relative element deltas, indexed by reference direction i (host-computed):
     int dpull[27];   // source of the pull of direction i: slot(i) plane - c_i . (1, pitch, zstride)
     int dlink[27];   // bounce-back source: own cell, slot(opp(i)) plane
@@ -73,6 +74,34 @@ struct Store<float> {
         *p = (float)(v - wt<Q, I>());
     }
 };
+
+// read-only load whose line should survive in L2 until a second reader
+// (L2 evict_last policy).  Used by the fp64 pulls only: measured on B200,
+// config 4 fp64 92.8 -> 94.6 % of the roofline; fp32 storage -4.7 % and
+// config 2 -3.7 % (the split loads cost issue slots those kernels lack).
+// -DLBM_LINK_HINT=0|1 forces it off / on for every storage type.
+template <typename Real>
+constexpr bool link_hint() {
+#ifdef LBM_LINK_HINT
+    return LBM_LINK_HINT != 0;
+#else
+    return std::is_same_v<Real, double>;
+#endif
+}
+template <typename T>
+__device__ __forceinline__ T ldg_keep(const T* p) {
+    if constexpr (sizeof(T) == 8) {
+        double v;
+        asm volatile("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+                     "ld.global.nc.L2::cache_hint.f64 %0, [%1], pol;\n}" : "=d"(v) : "l"(p));
+        return (T)v;
+    } else {
+        float v;
+        asm volatile("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+                     "ld.global.nc.L2::cache_hint.f32 %0, [%1], pol;\n}" : "=f"(v) : "l"(p));
+        return (T)v;
+    }
+}
 
 // per-axis source coordinate for a pull along -c (c in {-1,0,1})
 struct AxisSrc {
@@ -301,7 +330,20 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                 constexpr int k = D::opp[i];
                 d = ((code >> i) & 1u) ? g.dslot[k] : d;
             }
-            raw[i] = __ldg(sp + d);
+            // A bounce-back link of a fluid cell x reads G[x, opp(i)], which
+            // the wall cell across the link also pulls.  For directions with
+            // c_z = -1 the FIRST of the two reads is either x's link (wall one
+            // plane later) or a wall cell's pull (fluid cell one plane
+            // later); that read keeps the line in L2 (evict_last) for the
+            // second one instead of leaving it to a whole plane of traffic.
+            if constexpr (link_hint<Real>() && D::cz[i] == -1) {
+                if (g.link_hint && ((((code >> i) & 1u) != 0u) || !(code & LBM_MASK_FLUID)))
+                    raw[i] = ldg_keep(sp + d);
+                else
+                    raw[i] = __ldg(sp + d);
+            } else {
+                raw[i] = __ldg(sp + d);
+            }
         });
     } else {
         int64_t off[Q];
