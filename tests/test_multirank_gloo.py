@@ -154,3 +154,15 @@ def test_transport_selection_on_cpu_ranks():
     # CPU tensors over gloo: the host-staged transport; threads: the fused one
     assert P.run(2, _select_prog, backend="gloo") == ["staged", "staged"]
     assert P.run(2, _select_prog, backend="threads", device="cpu") == ["peer-device"] * 2
+
+
+def test_transport_env_is_validated(monkeypatch):
+    class _Lat:
+        pass
+    lat = _Lat()
+    lat.ctx, lat.device = P.Context(device="cpu"), torch.device("cpu")
+    monkeypatch.setenv("LBM_B200_HALO", "carrier-pigeon")
+    with pytest.raises(ValueError, match="LBM_B200_HALO"):
+        halo.select_transport(lat)
+    monkeypatch.setenv("LBM_B200_HALO", "nccl")
+    assert halo.select_transport(lat) == "staged"      # single process: nothing to exchange
