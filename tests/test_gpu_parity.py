@@ -532,3 +532,16 @@ def test_stream_flag_signal_orders_a_second_stream(api):
     torch.cuda.synchronize()
     assert float(out.min()) == 3.0 and float(out.max()) == 3.0
     assert int(flag.item()) == 1
+
+
+def test_fused_peer_halo_typed_links_two_thread_ranks(api):
+    """D3Q27 raw-moment MRT cavity with the UBB lid, split over 2 z-slab
+    thread ranks: dense-MRT peer instantiation, typed (UBB) links and wall
+    links next to the halo planes - bitwise equal to 1 rank."""
+    import paper_1909_13772_b200 as P
+    spec = dict(cases.CASES["c2_d3q27_rawmrt_cavity"])
+    spec.update(dims=(8, 8, 12), root_dims=(1, 1, 2), steps=12, snapshots=(5, 12))
+    base = cases.run_case(api, _ctx(), spec)
+    multi = P.run(2, _rank_prog, spec, backend="threads", device="cuda", timeout=300)[0]
+    for s in spec["snapshots"]:
+        assert multi["pdf"][s].tobytes() == base["pdf"][s].tobytes(), s
