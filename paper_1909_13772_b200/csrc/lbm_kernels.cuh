@@ -103,6 +103,8 @@ __device__ __forceinline__ T ldg_keep(const T* p) {
     }
 }
 
+// (Measured and dropped: L2::128B / L2::256B prefetch-size qualifiers on the
+// pulls - within noise on configs 4 fp64 / fp32 and 2.)
 // per-axis source coordinate for a pull along -c (c in {-1,0,1})
 struct AxisSrc {
     int lo_raw, hi_raw;    // coordinate - 1, coordinate + 1 (ghost-inclusive: may be -1 / n)
