@@ -105,6 +105,9 @@ __device__ __forceinline__ T ldg_keep(const T* p) {
 
 // (Measured and dropped: L2::128B / L2::256B prefetch-size qualifiers on the
 // pulls - within noise on configs 4 fp64 / fp32 and 2.)
+// (Measured and dropped: choosing the keep policy per warp - any wall lane
+// or link in the warp - so each direction stays one load instruction: the
+// extra evict_last lines cost 9 % in fp32 and nothing was gained in fp64.)
 // per-axis source coordinate for a pull along -c (c in {-1,0,1})
 struct AxisSrc {
     int lo_raw, hi_raw;    // coordinate - 1, coordinate + 1 (ghost-inclusive: may be -1 / n)
