@@ -11,6 +11,7 @@ for spec in "c4 f32" "c3 f64" "c1 f64" "c2 f32" "c0 f64"; do
   timeout 900 python bench.py --config $1 --dtype $2 --steps 100 --warmup 5 > gpurun_out/final_bench_$1_$2.log 2>&1; echo bench_$1_$2=$?
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/final_bench_reference.log 2>&1; echo ref=$?
+[ -n "$BENCH_ONLY" ] && exit 0
 CMD="python bench.py --profile --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/final_plain_c4.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches_c4_f64.csv $CMD > /dev/null 2>&1; echo launches=$?
