@@ -281,11 +281,21 @@ class PeerHalo:
         return base + offset
 
     def close(self):
-        """Unmap the neighbours' buffers (collective: nobody may still write)."""
+        """Unmap the neighbours' buffers.  Only this rank's stores go through
+        the mappings, so closing needs no collective - but no further phase
+        may run on this halo."""
         opened, self._opened = getattr(self, "_opened", {}), {}
         for base in opened.values():
             _lib.call("lbm_ipc_close", ctypes.c_void_p(base))
         self.peer = {}
+
+    def __del__(self):
+        # the lattice (and this halo) goes away: drop the IPC mappings so a
+        # neighbour's freed buffer is not kept alive by this process
+        try:
+            self.close()
+        except Exception:
+            pass
 
     # -- protocol
     def _enter_phase(self, stream):
