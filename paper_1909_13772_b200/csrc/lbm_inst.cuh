@@ -13,6 +13,7 @@
 #include "lbm_vec.cuh"
 #endif
 
+
 #ifndef LBM_REAL
 #error "define LBM_REAL before including lbm_inst.cuh"
 #endif
