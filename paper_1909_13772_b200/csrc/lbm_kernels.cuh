@@ -328,13 +328,8 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
         static_for<0, Q>([&](auto I_) {
             constexpr int i = decltype(I_)::value;
             int d = g.dpull[i];
-            // link source = own cell, slot opp(i): the store delta of opp(i)
-            // (KGrid::dlink[i] == dslot[opp(i)]), so the select reuses the
-            // constant the store phase loads anyway
-            if constexpr (i > 0) {
-                constexpr int k = D::opp[i];
-                d = ((code >> i) & 1u) ? g.dslot[k] : d;
-            }
+            // link source = own cell, slot opp(i) (KGrid::dlink)
+            if constexpr (i > 0) d = ((code >> i) & 1u) ? g.dlink[i] : d;
             // A bounce-back link of a fluid cell x reads G[x, opp(i)], which
             // the wall cell across the link also pulls.  For directions with
             // c_z = -1 the FIRST of the two reads is either x's link (wall one
