@@ -214,21 +214,29 @@ class PeerHalo:
         peers = ctx.all_gather(info)
         self.peer = {}          # face -> addresses (buf0, buf1, flags) of the neighbour across it
         self.peer_info = {}
-        for face, peer, facing in ((0, box.lo_peer, 1), (1, box.hi_peer, 0)):
-            zmode = box.zface_lo if face == 0 else box.zface_hi
-            if zmode != _lib.ZFACE_HALO:
-                continue
-            pi = peers[peer]
-            if (pi["pitch"], pi["rb"], pi["q"]) != (lat.grid.pitch, lat.real_bytes, lat.q):
-                raise RuntimeError("z-neighbours disagree on the row layout")
-            if in_process:
-                addrs = table[peer]
-            else:
-                addrs = tuple(self._open(h, off) for h, off in pi["handles"])
-            self.peer[face] = addrs
-            self.peer_info[face] = (pi["blocks"][facing], pi["spans"][facing])
+        err = None
+        try:
+            for face, peer, facing in ((0, box.lo_peer, 1), (1, box.hi_peer, 0)):
+                zmode = box.zface_lo if face == 0 else box.zface_hi
+                if zmode != _lib.ZFACE_HALO:
+                    continue
+                pi = peers[peer]
+                if (pi["pitch"], pi["rb"], pi["q"]) != (lat.grid.pitch, lat.real_bytes, lat.q):
+                    raise RuntimeError("z-neighbours disagree on the row layout")
+                if in_process:
+                    addrs = table[peer]
+                else:
+                    addrs = tuple(self._open(h, off) for h, off in pi["handles"])
+                self.peer[face] = addrs
+                self.peer_info[face] = (pi["blocks"][facing], pi["spans"][facing])
+        except Exception as exc:    # decided collectively below, never a lone raise
+            err = f"rank {ctx.rank}: {type(exc).__name__}: {exc}"
         self.bytes_per_exchange = sum(self.spans[f][2] for f in self.peer) * lat.real_bytes
-        ctx.barrier()   # every rank holds its peers' mappings before any phase
+        # every rank holds its peers' mappings before any phase (or all fall back)
+        errs = [e for e in ctx.all_gather(err).values() if e]
+        if errs:
+            self.close()
+            raise PeerHaloUnavailable("; ".join(errs))
         if mode == "device":
             self._handshake()
 

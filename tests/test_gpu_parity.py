@@ -545,3 +545,38 @@ def test_fused_peer_halo_typed_links_two_thread_ranks(api):
     multi = P.run(2, _rank_prog, spec, backend="threads", device="cuda", timeout=300)[0]
     for s in spec["snapshots"]:
         assert multi["pdf"][s].tobytes() == base["pdf"][s].tobytes(), s
+
+
+def _rank_prog_broken_ipc(ctx, spec):
+    import warnings
+    from paper_1909_13772_b200 import device, halo
+    if ctx.rank == 1:
+        def broken(self, handle, offset):
+            raise RuntimeError("simulated IPC failure")
+        halo.PeerHalo._open = broken
+    kinds = []
+    make = halo.make_halo
+
+    def recording(lat):
+        h = make(lat)
+        kinds.append(h.kind)
+        return h
+    halo.make_halo = recording
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
+        res = cases.run_case(cases.b200_api(), ctx, spec)
+    fell_back = any("fused peer halo unavailable" in str(w.message) for w in caught)
+    return res, kinds, fell_back
+
+
+def test_fused_peer_halo_setup_failure_falls_back_collectively(api, monkeypatch):
+    """One rank failing to map its neighbour makes EVERY rank fall back to
+    the send/recv transport (no lone raise, no hang); results stay bitwise."""
+    import paper_1909_13772_b200 as P
+    monkeypatch.setenv("LBM_B200_HALO", "peer")
+    spec = dict(_HALO_SPEC, root_dims=(1, 1, 2), snapshots=(12,))
+    per_rank = P.run(2, _rank_prog_broken_ipc, spec, backend="gloo", device="cuda")
+    for res, kinds, fell_back in per_rank:
+        assert kinds == ["staged"] and fell_back
+    base = cases.run_case(api, _ctx(), spec)
+    assert per_rank[0][0]["pdf"][12].tobytes() == base["pdf"][12].tobytes()
