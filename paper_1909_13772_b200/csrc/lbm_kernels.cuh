@@ -402,7 +402,7 @@ __device__ __forceinline__ void pull_finish(const KGrid& g, const KParams& p,
 // config 4 D3Q19 TRT fp64: minb 1 -> 83 %, 5 -> 89 %, 6 -> 91.9 %,
 // 7 -> 92.4 %, 8 -> 89.7 % of the HBM roofline).  MRT keeps all registers.
 // -DLBM_FUSED_MINB=n overrides for tuning builds.
-template <int Q, typename Real, int MODEL>
+template <int Q, typename Real, int MODEL, int FORCE = 0>
 constexpr int fused_minb() {
     if constexpr (std::is_same_v<Real, float>) {
         if constexpr (MODEL == 3) {
@@ -422,7 +422,10 @@ constexpr int fused_minb() {
 #ifdef LBM_FUSED_MINB
         return LBM_FUSED_MINB;
 #else
-        return MODEL == 2 ? 1 : (Q == 9 ? 8 : (Q == 19 ? 6 : 4));
+        // D3Q19 SRT/TRT fp64: 6 (config 3, no force); with Guo 7 (config 4:
+        // 6 -> 93.3 %, 7 -> 94.3 %, 5 -> 89.6 %, measured with the link hint)
+        constexpr bool guo = FORCE == 1 || FORCE == 3;
+        return MODEL == 2 ? 1 : (Q == 9 ? 8 : (Q == 19 ? (guo && MODEL <= 1 ? 7 : 6) : 4));
 #endif
     }
 }
@@ -455,9 +458,9 @@ __device__ __forceinline__ void store_any(Real* p, Acc v) {
 #ifndef LBM_FUSED_BX
 #define LBM_FUSED_BX 128
 #endif
-template <int Q, typename Real, int MODEL>
+template <int Q, typename Real, int MODEL, int FORCE = 0>
 constexpr int fused_minb_bx() {
-    constexpr int m = fused_minb<Q, Real, MODEL>() * 128 / LBM_FUSED_BX;
+    constexpr int m = fused_minb<Q, Real, MODEL, FORCE>() * 128 / LBM_FUSED_BX;
     return m < 1 ? 1 : m;
 }
 
@@ -468,7 +471,7 @@ constexpr int fused_minb_bx() {
 // a tile first, to bring the z-neighbour that re-reads a bounce-back source
 // closer in time: -1..-8 % on configs 4 fp64 / fp32 and 2.)
 template <int Q, typename Real, int MODEL, int FORCE, bool MOVING = false, bool PEER = false>
-__global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL>())
+__global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FORCE>())
     k_fused(KGrid g, KParams p, const Real* __restrict__ src,
                                                Real* __restrict__ dst,
                                                const uint32_t* __restrict__ cellmask,
