@@ -28,6 +28,8 @@
  *                       (field/core.py:34-70; "fzyx" raw shape (q,Z,Y,X)).
  *   lbm_build_cellmask  build_index_lists + sweep-time flag validation
  *                       (lbm/boundary.py:48-97, lbm/sweep.py:124-136).
+ *   lbm_refresh_fluid_mask  the per-sweep fluid mask of flags edited after
+ *                       freeze() (lbm/sweep.py:124-136; links stay frozen).
  *   lbm_collide_cells / lbm_equilibrium_cells / lbm_macroscopic_cells
  *                       collide_pdfs / equilibrium / macroscopic on flat
  *                       (n, q) populations (lbm/collision.py:138-184,245-261).
@@ -40,6 +42,13 @@
  *                       store their crossing directions into the
  *                       neighbour's ghost plane (peer HBM over NVLink);
  *                       lbm_stream_signal / lbm_stream_wait order the phases.
+ *   lbm_slot_collide / lbm_slot_stream_pull  the kernel slot itself,
+ *                       impl.collide / impl.stream_pull
+ *                       (_kernels/__init__.py:10-37, _core_py.py:70-218) on
+ *                       dense (z, y, x, q) arrays, ghost ring included - the
+ *                       per-call "b200" backend of blocksim._kernels.
+ *   lbm_bind_params     re-binds a parameter block's device-side state (MRT
+ *                       constant tables) before a captured CUDA graph replays.
  *   lbm_face_span       geometry of the per-step z-face ghost exchange
  *                       (field/ghost.py:112-173,202-264), restricted to the
  *                       PDF directions that cross the face.
@@ -50,9 +59,13 @@
  * with plane = (ny+2) * pitch and slot = lbm_slot_of(q, i).  Direction i is stored in slot
  * lbm_slot_of(q, i): slots are grouped by c_z (-1, 0, +1), so the directions
  * that cross a z-face form ONE contiguous run per z-plane and the halo can be
- * sent straight out of / into the field (zero-copy NCCL send/recv).
- * real_bytes == 8 stores f in fp64; real_bytes == 4 stores (f - w_i) in fp32
- * and computes in fp64 registers.
+ * stored straight into the neighbour's ghost plane by the boundary-plane
+ * kernel (lbm_fused_step_peer) or sent out of / into the field by NCCL
+ * without a pack kernel.
+ * real_bytes == 8 stores f in fp64 and computes in fp64 (bitwise reference
+ * arithmetic); real_bytes == 4 stores the centred populations (f - w_i) in
+ * fp32 and computes in fp32 registers on the centred values (FMA allowed;
+ * checked against the fp64 path at 1e-5 relative).
  */
 #ifndef LBM_B200_H
 #define LBM_B200_H
@@ -64,7 +77,7 @@
 extern "C" {
 #endif
 
-#define LBM_B200_ABI_VERSION 4
+#define LBM_B200_ABI_VERSION 5
 
 /* status codes */
 #define LBM_OK 0
@@ -102,7 +115,7 @@ extern "C" {
 
 typedef struct lbm_grid {
     int q;          /* 9, 19 or 27                                  */
-    int real_bytes; /* 8 (fp64) or 4 (fp32 storage of f - w_i)      */
+    int real_bytes; /* 8 (fp64) or 4 (fp32 storage and arithmetic on f - w_i) */
     int nx, ny, nz; /* interior cells of this rank's box            */
     int pitch;      /* elements per x row (>= xoff + nx + 1)        */
     int xoff;       /* element offset of interior x = 0 in a row (>= 1) */
@@ -280,6 +293,16 @@ int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags,
                        const uint32_t bits[5], uint32_t* cellmask,
                        uint32_t* typemask, int* err, void* stream);
 
+/* Sweep-time collision mask (ABI 5): links stay as frozen by
+ * lbm_build_cellmask at BoundaryHandling.freeze() (boundary.py:128-131), the
+ * fluid bit follows the CURRENT flags (lbm/sweep.py:124-136: the reference
+ * collides `flags & Fluid` of the sweep's own flags).  cellmask_out =
+ * cellmask_in with LBM_MASK_FLUID recomputed from flags (Z, Y, X).  err
+ * (device int, caller sets INT_MAX): first unflagged interior cell + 1. */
+int lbm_refresh_fluid_mask(const lbm_grid_t* g, const uint32_t* flags,
+                           const uint32_t bits[5], const uint32_t* cellmask_in,
+                           uint32_t* cellmask_out, int* err, void* stream);
+
 /* Combined masks of a moving-body sweep: cellmask_out = cellmask_in with
  * LBM_MASK_FLUID cleared on covered cells (owner >= 0; they skip the
  * collision, coupling/sweep.py:107-110) and, on the remaining fluid cells,
@@ -298,6 +321,30 @@ int lbm_equilibrium_cells(int q, const double* rho, const double* u,
 int lbm_macroscopic_cells(int q, const lbm_params_t* p, const double* f,
                           double* rho, double* u, int* bad_count, int64_t n,
                           void* stream);
+
+/* Validate (g, p) and make the current device hold p's constant-memory
+ * state (MRT tables; uploaded on `stream` only when the device holds other
+ * content).  Every launch entry point does this itself; call it before
+ * replaying a CUDA graph that captured launches with p (ABI 5). */
+int lbm_bind_params(const lbm_grid_t* g, const lbm_params_t* p, void* stream);
+
+/* ------------------------------------------ kernel slot (ABI 5) */
+/* impl.collide (_core_py.py:70-200) on dense (n, q) fp64 populations in
+ * place (a (z, y, x, q) box flattened, ghost ring included): cell c is
+ * collided when flags[c] & fluid_bits != 0.  p->model == LBM_SRT_FIELD
+ * reads the per-cell rate from p->omega_cells[c] (the omega_window).
+ * All arrays are DEVICE pointers. */
+int lbm_slot_collide(int q, const lbm_params_t* p, double* f,
+                     const uint32_t* flags, uint32_t fluid_bits, int64_t n,
+                     void* stream);
+/* impl.stream_pull (_core_py.py:203-218): src is a dense ghost-inclusive
+ * (nzg, nyg, nxg, q) fp64 box with gl ghost layers (device); out receives
+ * the interior (nzg-2gl, nyg-2gl, nxg-2gl, q) with
+ * out[z, y, x, i] = src[z+gl-cz[i], y+gl-cy[i], x+gl-cx[i], i].  cx/cy/cz
+ * are HOST int32 arrays of length q (the caller's velocity set). */
+int lbm_slot_stream_pull(int q, const int32_t* cx, const int32_t* cy,
+                         const int32_t* cz, const double* src, double* out,
+                         int nxg, int nyg, int nzg, int gl, void* stream);
 
 #ifdef __cplusplus
 }

@@ -262,14 +262,18 @@ void orc_exchange_u32(uint32_t* data, int X, int Y, int Z, const int periodic[3]
  * exchanged ghost flags (BoundaryHandling.freeze).  links may be NULL
  * (fully periodic, no handling: every cell collides, sweep.py:333-334).
  * Returns 0. */
+/* link_flags: the flags the links were frozen from (BoundaryHandling.freeze,
+ * boundary.py:128-131); `flags` are the current ones the collision reads
+ * (lbm/sweep.py:124-136).  NULL: the same array. */
 int orc_run(const orc_stencil* st, double* a, double* b, const uint32_t* flags,
-            uint32_t fluid_bits, int X, int Y, int Z, const int periodic[3],
-            const orc_params* p, const orc_links* links, int steps) {
+            const uint32_t* link_flags, uint32_t fluid_bits, int X, int Y, int Z,
+            const int periodic[3], const orc_params* p, const orc_links* links, int steps) {
+    if (!link_flags) link_flags = flags;
     for (int s = 0; s < steps; ++s) {
         orc_exchange(a, st->q, X, Y, Z, periodic);
         orc_collide(st, a, flags, fluid_bits, X, Y, Z, p);
         orc_stream_pull(st, a, b, X, Y, Z);
-        if (links) orc_apply_links(st, a, b, flags, X, Y, Z, links);
+        if (links) orc_apply_links(st, a, b, link_flags, X, Y, Z, links);
         /* swap: copy back so `a` stays the src handle for the caller */
         double* t = a;
         a = b;

@@ -218,7 +218,7 @@ def lib():
                             % str(here.parent)], check=True)
         _lib = ctypes.CDLL(str(LIB_PATH))
         P = ctypes.c_void_p
-        _lib.orc_run.argtypes = [P, P, P, P, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
+        _lib.orc_run.argtypes = [P, P, P, P, P, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_int, P, P, P, ctypes.c_int]
         _lib.orc_run.restype = ctypes.c_int
         _lib.orc_collide.argtypes = [P, P, P, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
@@ -308,6 +308,7 @@ class Domain:
             # BoundaryHandling.freeze: exchange flag ghosts (boundary.py:128-131)
             lib().orc_exchange_u32(_ptr(self.flags), self.X, self.Y, self.Z, _ptr(self.periodic))
             self.fluid_bits = int(bits["Fluid"])
+            self.bits = dict(bits)
             L = _Links()
             L.fluid, L.noslip, L.ubb = int(bits["Fluid"]), int(bits["NoSlip"]), int(bits["UBB"])
             L.pressure = int(bits["Pressure"])
@@ -321,7 +322,17 @@ class Domain:
             lib().orc_exchange(_ptr(of), 1, self.X, self.Y, self.Z, _ptr(self.periodic))
             model.omega_field = of
         self._cp = model.cparams()
+        self.link_flags = None
         self.steps = 0
+
+    def edit_flag(self, x, y, z, name):
+        """Set interior cell (x, y, z) to flag `name` WITHOUT re-freezing:
+        the links stay those of the initial flags (boundary.py:128-131), the
+        collision reads the edited flags (lbm/sweep.py:124-136); ghost flags
+        keep their last exchange, as in the reference."""
+        if self.link_flags is None:
+            self.link_flags = self.flags.copy()
+        self.flags[z + 1, y + 1, x + 1] = self.bits[name]
 
     def set_full(self, pdf_qzyx):
         self.a[...] = pdf_qzyx
@@ -330,7 +341,7 @@ class Domain:
     def run(self, steps):
         L = lib()
         odd = L.orc_run(ctypes.byref(self._cst), _ptr(self.a), _ptr(self.b), _ptr(self.flags),
-                        self.fluid_bits, self.X, self.Y, self.Z, _ptr(self.periodic),
+                        _ptr(self.link_flags), self.fluid_bits, self.X, self.Y, self.Z, _ptr(self.periodic),
                         ctypes.byref(self._cp),
                         ctypes.byref(self.links) if self.links is not None else None, int(steps))
         if odd:

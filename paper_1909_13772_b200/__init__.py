@@ -5,8 +5,11 @@ ensure_flags, BoundaryHandling, fill_equilibrium, stream_collide,
 exchange_ghosts, macroscopic_fields, gather_slice, mlups; forest snapshots
 and VTK output) whose compute runs
 in hand-written sm_100a kernels (csrc/, C-ABI include/lbm_b200.h) on
-HBM-resident structure-of-arrays PDF fields, z-slab partitioned over GPUs
-with a zero-copy NCCL halo of the crossing directions.
+HBM-resident structure-of-arrays PDF fields, z-slab partitioned over GPUs.
+The per-step halo of the crossing directions is fused into the boundary
+planes' kernel, which stores them into the neighbour's ghost plane (peer
+HBM over NVLink, CUDA IPC); NCCL send/recv of the contiguous runs is the
+fallback transport (halo.py).
 """
 from .errors import BackendError, BlocksimError, BufferUnderflowError, NumericsError, \
     SyncError, TopologyError, TypeTagError, ValidationError

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
 
 LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
 ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
-ABI_VERSION = 4
+ABI_VERSION = 5
 SRT, TRT, MRT, SRT_FIELD = 0, 1, 2, 3
 MASK_FLUID = 0x1
 MASK_UBB = 0x80000000
@@ -31,6 +31,7 @@ EXPORTS = (
     "lbm_build_moving_masks", "lbm_fused_step_peer", "lbm_ghost_block_offset",
     "lbm_stream_signal", "lbm_stream_wait", "lbm_copy_async",
     "lbm_ipc_export", "lbm_ipc_open", "lbm_ipc_close",
+    "lbm_bind_params", "lbm_slot_collide", "lbm_slot_stream_pull", "lbm_refresh_fluid_mask",
 )
 
 
@@ -108,6 +109,10 @@ def load(path: Path | None = None):
         "lbm_ipc_export": ([P, P, ctypes.POINTER(I64)], I),
         "lbm_ipc_open": ([P, ctypes.POINTER(P)], I),
         "lbm_ipc_close": ([P], I),
+        "lbm_bind_params": ([G, PR, P], I),
+        "lbm_slot_collide": ([I, PR, P, P, ctypes.c_uint32, I64, P], I),
+        "lbm_slot_stream_pull": ([I, P, P, P, P, P, I, I, I, I, P], I),
+        "lbm_refresh_fluid_mask": ([G, P, P, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

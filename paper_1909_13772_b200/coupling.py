@@ -238,8 +238,7 @@ def moving_boundary_sweep(pdf, model, mapping, *, handling=None, force=None, bod
         for block in forest.local_blocks():
             if block.data[handling.flags_key].g != pdf.g:
                 raise ValidationError("flag and pdf ghost layers differ")
-        handling.check_flags()
-        static = handling.masks
+        static = handling.sweep_masks()
         if static.unflagged_cell is not None:
             raise ValidationError(f"unflagged cell {static.unflagged_cell}")
     else:

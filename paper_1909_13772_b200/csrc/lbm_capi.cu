@@ -7,6 +7,7 @@
 // (compiled with -fmad=false like the fp64 unit).
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <cuda.h>
@@ -69,7 +70,12 @@ int check_grid(const lbm_grid_t* g, KGrid* k) {
     k->zhi = g->zface_hi;
     k->plane = (int64_t)(g->ny + 2) * g->pitch;
     k->zstride = (int64_t)g->q * k->plane;
-    if ((int64_t)(g->q + 2) * k->plane >= ((int64_t)1 << 31))
+    // the kernels address a cell's sources and stores as int32 deltas from
+    // the cell (KGrid::dpull/dlink/dslot, peer stores): every delta is
+    // computed in int64 below and range-checked before it is narrowed; the
+    // plane and z-stride themselves must fit too
+    const int64_t lim = ((int64_t)1 << 31) - 1;
+    if (k->zstride > lim)
         return fail(LBM_EINVAL, "x-y plane of %lld elements too large for 32-bit in-plane offsets",
                     (long long)k->plane);
     k->plane32 = (int)k->plane;
@@ -78,19 +84,34 @@ int check_grid(const lbm_grid_t* g, KGrid* k) {
     // the field is large against L2 (measured: +1.9 % on config 4 at 512^2,
     // -1.2 % on config 1 at 128^2 where the re-reads hit anyway)
     k->link_hint = k->zstride * g->real_bytes >= ((int64_t)16 << 20) ? 1 : 0;
+    // LBM_B200_LINK_HINT=0|1 forces the choice (tests run the evict_last
+    // path on small grids; it changes cache policy only, never a value)
+    if (const char* h = getenv("LBM_B200_LINK_HINT")) {
+        if (h[0] == '0' || h[0] == '1') k->link_hint = h[0] - '0';
+    }
+    bool fits = true;
+    auto narrow = [&](int64_t v) {
+        if (v > lim || v < -lim) fits = false;
+        return (int)v;
+    };
     auto fill = [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         using D = Dirs<Q>;
         for (int i = 0; i < 27; ++i) k->dpull[i] = k->dlink[i] = k->dslot[i] = 0;
         for (int i = 0; i < Q; ++i) {
-            k->dslot[i] = slot_of<Q>(i) * k->plane32;
-            k->dpull[i] = k->dslot[i] - D::cz[i] * k->zstride32 - D::cy[i] * g->pitch - D::cx[i];
-            k->dlink[i] = slot_of<Q>(D::opp[i]) * k->plane32;
+            const int64_t slot = (int64_t)slot_of<Q>(i) * k->plane;
+            k->dslot[i] = narrow(slot);
+            k->dpull[i] = narrow(slot - D::cz[i] * k->zstride - D::cy[i] * (int64_t)g->pitch - D::cx[i]);
+            k->dlink[i] = narrow((int64_t)slot_of<Q>(D::opp[i]) * k->plane);
         }
     };
     if (g->q == 9) fill(std::integral_constant<int, 9>{});
     else if (g->q == 19) fill(std::integral_constant<int, 19>{});
     else fill(std::integral_constant<int, 27>{});
+    // (peer stores add dslot < zstride to an int64 row offset: covered above)
+    if (!fits)
+        return fail(LBM_EINVAL, "x-y plane of %lld elements too large for 32-bit in-plane offsets",
+                    (long long)k->plane);
     return LBM_OK;
 }
 
@@ -299,6 +320,22 @@ __global__ void k_moving_masks(KGrid g, const uint32_t* __restrict__ cm_in,
     if (n) atomicAdd(n_links, n);
 }
 
+// Sweep-time fluid mask (lbm/sweep.py:124-136): links stay as frozen at
+// freeze() (boundary.py:128-131), the collision mask follows the CURRENT
+// flags; err[0] = first unflagged interior cell + 1.
+__global__ void k_refresh_fluid(KGrid g, const uint32_t* __restrict__ flags, uint32_t fluid,
+                                uint32_t known, const uint32_t* __restrict__ cm_in,
+                                uint32_t* __restrict__ cm_out, int* err) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    const uint32_t f = flags[((int64_t)(z + 1) * (g.ny + 2) + (y + 1)) * (g.nx + 2) + (x + 1)];
+    if ((f & known) == 0u) note_first(&err[0], cell);
+    cm_out[cell] = (cm_in[cell] & ~LBM_MASK_FLUID) | ((f & fluid) ? LBM_MASK_FLUID : 0u);
+}
+
 // ------------------------------------------------------------ flat cells
 template <int Q, int MODEL, int FORCE>
 __global__ void k_collide_cells(KParams p, double* __restrict__ f, int64_t n) {
@@ -310,6 +347,48 @@ __global__ void k_collide_cells(KParams p, double* __restrict__ f, int64_t n) {
     collide_cell<Q, MODEL, FORCE>(v, p);
 #pragma unroll
     for (int i = 0; i < Q; ++i) f[c * Q + i] = v[i];
+}
+
+// Kernel-slot collide (impl.collide, _core_py.py:70-200): every cell of a
+// dense (n, q) population array whose flags & fluid_bits != 0, ghost ring
+// included; MODEL 4 reads the per-cell rate (the omega_window of an SRT
+// rate field).
+template <int Q, int MODEL, int FORCE>
+__global__ void k_slot_collide(KParams p, double* __restrict__ f, const uint32_t* __restrict__ flags,
+                               uint32_t fluid_bits, const double* __restrict__ omega, int64_t n) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n || (flags[c] & fluid_bits) == 0u) return;
+    double v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) v[i] = f[c * Q + i];
+    double om = 0.0;
+    if constexpr (MODEL == 4) om = omega[c];
+    collide_cell<Q, MODEL, FORCE>(v, p, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[c * Q + i] = v[i];
+}
+
+// Kernel-slot pull (impl.stream_pull, _core_py.py:203-218): dense (Z, Y, X, q)
+// ghost-inclusive src with `gl` ghost layers -> interior (nz, ny, nx, q),
+// out[z, y, x, i] = src[z + gl - cz_i, y + gl - cy_i, x + gl - cx_i, i] for
+// the caller's velocity set (passed as given, not assumed).
+struct SlotStencil {
+    int cx[27], cy[27], cz[27];
+};
+
+__global__ void k_slot_stream_pull(SlotStencil c, int q, const double* __restrict__ src,
+                                   double* __restrict__ out, int X, int Y, int gl, int nx, int ny,
+                                   int nz) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= nx) return;
+    const int64_t o = (((int64_t)z * ny + y) * nx + x) * q;
+    for (int i = 0; i < q; ++i) {
+        const int64_t s = (((int64_t)(z + gl - c.cz[i]) * Y + (y + gl - c.cy[i])) * X +
+                           (x + gl - c.cx[i])) * q + i;
+        out[o + i] = src[s];
+    }
 }
 
 template <int Q>
@@ -700,6 +779,22 @@ int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags, const uint32_
     return cuda_status(e, "lbm_build_cellmask");
 }
 
+int lbm_refresh_fluid_mask(const lbm_grid_t* g, const uint32_t* flags, const uint32_t bits[5],
+                           const uint32_t* cellmask_in, uint32_t* cellmask_out, int* err,
+                           void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!flags || !bits || !cellmask_in || !cellmask_out || !err)
+        return fail(LBM_EINVAL, "NULL buffer");
+    const uint32_t known = bits[0] | bits[1] | bits[2] | bits[3] | bits[4];
+    cudaStream_t s = (cudaStream_t)stream;
+    dim3 blk = cell_block(g->nx);
+    dim3 grid((g->nx + blk.x - 1) / blk.x, g->ny, g->nz);
+    k_refresh_fluid<<<grid, blk, 0, s>>>(k, flags, bits[0], known, cellmask_in, cellmask_out, err);
+    return cuda_status(cudaGetLastError(), "lbm_refresh_fluid_mask");
+}
+
 int lbm_build_moving_masks(const lbm_grid_t* g, const uint32_t* cellmask_in, const int32_t* owner,
                            uint32_t* cellmask_out, uint32_t* linkmask, int* n_links, void* stream) {
     KGrid k;
@@ -790,6 +885,77 @@ int lbm_macroscopic_cells(int q, const lbm_params_t* p, const double* f, double*
         return cudaGetLastError();
     });
     return cuda_status(e, "lbm_macroscopic_cells");
+}
+
+int lbm_bind_params(const lbm_grid_t* g, const lbm_params_t* p, void* stream) {
+    KGrid k;
+    KParams kp;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    return check_params(p, g->q, &kp, (cudaStream_t)stream, g->real_bytes);
+}
+
+int lbm_slot_collide(int q, const lbm_params_t* p, double* f, const uint32_t* flags,
+                     uint32_t fluid_bits, int64_t n, void* stream) {
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!q_ok(q)) return fail(LBM_EINVAL, "q must be 9, 19 or 27, got %d", q);
+    if (!p) return fail(LBM_EINVAL, "params is NULL");
+    if (p->model == LBM_MRT) {
+        if (!p->mrt) return fail(LBM_EINVAL, "MRT needs its tables");
+        cudaError_t e = set_mrt_tables_capi(q, p->mrt, s);
+        if (e != cudaSuccess) return cuda_status(e, "MRT tables");
+    }
+    lbm_params_t copy = *p;
+    if (p->model == LBM_MRT) copy.model = LBM_SRT;   // tables already set above
+    int st = check_params(&copy, q, &kp, s, 8);
+    if (st != LBM_OK) return st;
+    if (n <= 0) return LBM_OK;
+    if (!f || !flags) return fail(LBM_EINVAL, "NULL buffer");
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+    const double* om = p->omega_cells;
+    cudaError_t e = by_q(q, [&](auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        const int m = p->model == LBM_SRT_FIELD ? 4 : p->model;
+        const int fm = p->force_mode;
+#define LBM_SLOT(M, F)                                                                        \
+    if (m == M && fm == F) {                                                                  \
+        k_slot_collide<Q, M, F><<<blocks, threads, 0, s>>>(kp, f, flags, fluid_bits, om, n);  \
+        return cudaGetLastError();                                                            \
+    }
+        LBM_SLOT(0, 0) LBM_SLOT(0, 1) LBM_SLOT(0, 2) LBM_SLOT(0, 3)
+        LBM_SLOT(1, 0) LBM_SLOT(1, 1) LBM_SLOT(1, 3)
+        LBM_SLOT(2, 0) LBM_SLOT(2, 1) LBM_SLOT(2, 3)
+        LBM_SLOT(4, 0) LBM_SLOT(4, 1) LBM_SLOT(4, 3)
+#undef LBM_SLOT
+        return cudaErrorInvalidValue;
+    });
+    return cuda_status(e, "lbm_slot_collide");
+}
+
+int lbm_slot_stream_pull(int q, const int32_t* cx, const int32_t* cy, const int32_t* cz,
+                         const double* src, double* out, int nxg, int nyg, int nzg, int gl,
+                         void* stream) {
+    if (q < 1 || q > 27) return fail(LBM_EINVAL, "q must be 1..27, got %d", q);
+    if (!cx || !cy || !cz || !src || !out) return fail(LBM_EINVAL, "NULL argument");
+    if (gl < 1) return fail(LBM_EINVAL, "stream_pull needs a ghost layer, got %d", gl);
+    const int nx = nxg - 2 * gl, ny = nyg - 2 * gl, nz = nzg - 2 * gl;
+    SlotStencil c;
+    for (int i = 0; i < q; ++i) {
+        if (cx[i] < -gl || cx[i] > gl || cy[i] < -gl || cy[i] > gl || cz[i] < -gl || cz[i] > gl)
+            return fail(LBM_EINVAL, "velocity %d reaches past %d ghost layer(s)", i, gl);
+        c.cx[i] = cx[i];
+        c.cy[i] = cy[i];
+        c.cz[i] = cz[i];
+    }
+    if (nx <= 0 || ny <= 0 || nz <= 0) return LBM_OK;
+    if (ny > 65535 || nz > 65535) return fail(LBM_EINVAL, "ny/nz too large for the launch grid");
+    cudaStream_t s = (cudaStream_t)stream;
+    dim3 blk = cell_block(nx);
+    dim3 grid((nx + blk.x - 1) / blk.x, ny, nz);
+    k_slot_stream_pull<<<grid, blk, 0, s>>>(c, q, src, out, nxg, nyg, gl, nx, ny, nz);
+    return cuda_status(cudaGetLastError(), "lbm_slot_stream_pull");
 }
 
 }  // extern "C"

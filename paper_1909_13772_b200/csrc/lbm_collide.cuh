@@ -14,6 +14,9 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <mutex>
+#include <vector>
+
 #include "lbm_stencil.cuh"
 
 namespace lbm {
@@ -52,23 +55,52 @@ struct KParams {
 };
 
 // MRT tables in constant memory: M, Minv, S, G (q <= 27).  One private copy
-// per translation unit (no -rdc); each unit exposes a setter that uploads
-// only when the content changed (tables are per model, not per step).
+// per translation unit (no -rdc) and per device (constant memory belongs to
+// the device's context); each unit exposes a setter that uploads only when
+// the device does not already hold the same content (tables are per model,
+// not per step).  The record of what each device holds is keyed by the
+// current device and guarded by a mutex, so rank threads driving different
+// GPUs (or one GPU) never skip an upload they need.  Captured CUDA graphs
+// do not capture constant memory: lbm_bind_params re-runs the setter before
+// a replay.
 #define LBM_MRT_MAXQ 27
 static __constant__ double c_mrt_M[LBM_MRT_MAXQ * LBM_MRT_MAXQ];
 static __constant__ double c_mrt_Minv[LBM_MRT_MAXQ * LBM_MRT_MAXQ];
 static __constant__ double c_mrt_S[LBM_MRT_MAXQ];
 static __constant__ double c_mrt_G[LBM_MRT_MAXQ * LBM_MRT_MAXQ];
 
+// per-device record of the last uploaded table content (+ one derived int)
+struct DeviceTableCache {
+    std::mutex mu;
+    std::vector<std::vector<double>> content;  // indexed by device ordinal
+    std::vector<int> derived;
+    // true (and *derived_out set) when device `dev` already holds `tables`
+    bool hit(int dev, const double* tables, size_t n, int* derived_out) {
+        if ((size_t)dev >= content.size()) {
+            content.resize(dev + 1);
+            derived.resize(dev + 1, 0);
+        }
+        const std::vector<double>& c = content[dev];
+        if (c.size() != n || memcmp(c.data(), tables, n * sizeof(double)) != 0) return false;
+        if (derived_out) *derived_out = derived[dev];
+        return true;
+    }
+    void store(int dev, const double* tables, size_t n, int d) {
+        content[dev].assign(tables, tables + n);
+        derived[dev] = d;
+    }
+};
+
 // tables: M[q*q] Minv[q*q] S[q] G[q*q] (G may be absent: pass zeros)
 #define LBM_DEFINE_MRT_SETTER(NAME)                                                       \
     cudaError_t NAME(int q, const double* tables, cudaStream_t s) {                       \
-        static double cache[3 * LBM_MRT_MAXQ * LBM_MRT_MAXQ + LBM_MRT_MAXQ];              \
-        static int cached_q = -1;                                                         \
+        static DeviceTableCache cache;                                                    \
         const size_t n = (size_t)3 * q * q + q;                                           \
-        if (cached_q == q && memcmp(cache, tables, n * sizeof(double)) == 0)              \
-            return cudaSuccess;                                                           \
-        cudaError_t e;                                                                    \
+        int dev = 0;                                                                      \
+        cudaError_t e = cudaGetDevice(&dev);                                              \
+        if (e != cudaSuccess) return e;                                                   \
+        std::lock_guard<std::mutex> lock(cache.mu);                                       \
+        if (cache.hit(dev, tables, n, nullptr)) return cudaSuccess;                       \
         const size_t qq = (size_t)q * q * sizeof(double);                                 \
         if ((e = cudaMemcpyToSymbolAsync(c_mrt_M, tables, qq, 0,                          \
                                          cudaMemcpyHostToDevice, s)) != cudaSuccess)       \
@@ -83,8 +115,7 @@ static __constant__ double c_mrt_G[LBM_MRT_MAXQ * LBM_MRT_MAXQ];
                                          cudaMemcpyHostToDevice, s)) != cudaSuccess)       \
             return e;                                                                     \
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;                      \
-        memcpy(cache, tables, n * sizeof(double));                                        \
-        cached_q = q;                                                                     \
+        cache.store(dev, tables, n, 0);                                                   \
         return cudaSuccess;                                                               \
     }
 

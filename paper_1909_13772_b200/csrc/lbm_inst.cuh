@@ -1,6 +1,7 @@
 // Launchers for one storage type.  Included by lbm_inst_f64.cu (REAL=double,
 // compiled with -fmad=false: bitwise reference arithmetic) and
-// lbm_inst_f32.cu (REAL=float storage, fp64 registers, FMA allowed).
+// lbm_inst_f32.cu (REAL=float storage of f - w_i, fp32 registers on the centred
+// populations, FMA allowed; readouts widen to fp64).
 #pragma once
 #include <stdlib.h>
 #include <string.h>

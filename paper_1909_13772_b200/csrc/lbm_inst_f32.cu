@@ -15,15 +15,15 @@ LBM_DEFINE_MRT_SETTER(set_mrt_tables_f32)
 // supports K = diagonal + one 3x3 block on (xx, yy, zz); with Guo forcing the
 // G table must equal Minv (I - S/2) M, i.e. R G Rinv = I - K/2 (checked).
 cudaError_t set_mrt_fast_f32(int q, const double* tables, cudaStream_t s, int* fast) {
-    static double cache[3 * 27 * 27 + 27];
-    static int cached = -1;
+    static DeviceTableCache cache;
     *fast = 0;
     if (q != 27) return cudaSuccess;
     const size_t n = 3 * 27 * 27 + 27;
-    if (cached >= 0 && memcmp(cache, tables, n * sizeof(double)) == 0) {
-        *fast = cached;
-        return cudaSuccess;
-    }
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    std::lock_guard<std::mutex> lock(cache.mu);
+    if (cache.hit(dev, tables, n, fast)) return cudaSuccess;
     const double* M = tables;
     const double* Minv = tables + 27 * 27;
     const double* S = tables + 2 * 27 * 27;
@@ -32,7 +32,10 @@ cudaError_t set_mrt_fast_f32(int q, const double* tables, cudaStream_t s, int* f
     // per-axis transform T1 (rows: power 0,1,2; cols: c = -1,0,1) and inverse
     const double T1[3][3] = {{1, 1, 1}, {-1, 0, 1}, {1, 0, 1}};
     const double T1i[3][3] = {{0, -0.5, 0.5}, {1, 0, -1}, {0, 0.5, 0.5}};  // [c][power]
-    static double R[27][27], Ri[27][27], A[27][27], C[27][27], K[27][27], H[27][27];
+    // (scratch on the heap of this call: several rank threads may derive at once)
+    std::vector<double> scratch(6 * 27 * 27);
+    auto R = reinterpret_cast<double(*)[27]>(scratch.data());
+    auto Ri = R + 27, A = R + 54, C = R + 81, K = R + 108, H = R + 135;
     for (int r = 0; r < 27; ++r) {
         const int a = r % 3, b = (r / 3) % 3, c = r / 9;
         for (int i = 0; i < 27; ++i) {
@@ -100,8 +103,7 @@ cudaError_t set_mrt_fast_f32(int q, const double* tables, cudaStream_t s, int* f
             return e;
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     }
-    memcpy(cache, tables, n * sizeof(double));
-    cached = ok;
+    cache.store(dev, tables, n, ok);
     *fast = ok;
     return cudaSuccess;
 }

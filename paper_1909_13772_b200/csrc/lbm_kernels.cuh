@@ -32,7 +32,7 @@ struct KGrid {
     int wrap_x, wrap_y, zlo, zhi;  // zlo/zhi: LBM_ZFACE_*
     int64_t plane;                 // (ny+2) * pitch
     int64_t zstride;               // q * plane
-    int plane32, zstride32;        // the same as int (the C-ABI checks (q+2) plane < 2^31)
+    int plane32, zstride32;        // the same as int (check_grid range-checks every delta)
     int link_hint;                 // 1: z-planes large against L2 (see ldg_keep)
     // own-relative element deltas, indexed by reference direction i (host-computed):
     int dpull[27];   // source of the pull of direction i: slot(i) plane - c_i . (1, pitch, zstride)
@@ -60,7 +60,9 @@ struct Store<double> {
     template <int Q, int I>
     __device__ __forceinline__ static void store(double* p, double v) { *p = v; }
 };
-// fp32: stored zero-centred (f - w_i), arithmetic in fp64 registers
+// fp32: stored zero-centred (f - w_i).  These widening accessors serve the
+// fp64-register readout kernels (stream-only, moments, convert); the fused
+// and collide-only kernels keep fp32 registers (AccOf<float>, lbm_collide_f32.cuh)
 template <>
 struct Store<float> {
     template <int Q, int I>

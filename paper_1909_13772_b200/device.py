@@ -13,7 +13,8 @@ the per-step schedule:
   planes concurrently on the caller's stream.  The boundary kernel stores
   its crossing directions straight into the z-neighbours' ghost planes
   (halo.PeerHalo: peer HBM over NVLink, ordered by stream flags); where the
-  ranks cannot map each other they go out by zero-copy NCCL send/recv.
+  ranks cannot map each other they go out by NCCL send/recv of the
+  contiguous runs (no pack kernel).
 
 Host<->device traffic happens only on upload (host R-form written by the
 user), readout (host arrays touched) and mask builds; never inside the step.
@@ -442,6 +443,10 @@ class DeviceLattice:
             # ping-pong returns to the same parity), odd remainder eagerly
             graph = self._pair_graph(kp, key, masks, cm, tm)
             if graph is not None:
+                # a graph captures kernel arguments, not constant memory:
+                # make the device hold this model's MRT tables again (another
+                # lattice may have uploaded its own since the capture)
+                _lib.call("lbm_bind_params", self.gref, kp.ref, self._sp(main))
                 for _ in range(nsteps // 2):
                     graph.replay()
                 pairs = nsteps // 2

@@ -163,6 +163,8 @@ class BoundaryHandling:
         exchange_ghosts(self.forest, [GhostPackInfo(self.flags_key)])
         self._masks = build_masks(self.forest, self.stencil, self.flags_key)
         self._flag_snapshot = self._dense_flags()
+        self._sweep_masks = self._masks
+        self._sweep_flags = self._flag_snapshot
         self._links = None
         self.generation += 1
         for block in self.forest.local_blocks():
@@ -203,19 +205,60 @@ class BoundaryHandling:
         return box.gather([b.data[self.flags_key].field.view_nosync for b in box.blocks], 1,
                           np.uint32)
 
-    def check_flags(self) -> None:
-        """Sweep-time guard: the masks are a snapshot of the flags taken at
-        freeze().  The reference re-reads the fluid mask every sweep but keeps
-        the frozen links; a mixed state cannot be expressed by one mask, so
-        edits after freeze() must be followed by another freeze()."""
+    def sweep_masks(self) -> Masks:
+        """The masks of the next sweep.  As in the reference, the links are
+        the ones frozen at freeze() (boundary.py:128-131, sweep.py:107-108),
+        while the collision follows the CURRENT flags and an unflagged
+        interior cell is rejected (sweep.py:124-136): flags edited after
+        freeze() keep the frozen link bits and get the fluid bit of their
+        current flags (lbm_refresh_fluid_mask).  Only a host access to the
+        flag fields triggers the comparison.
+
+        One reference quirk is not reproduced: the reference collides the
+        ghost images of a cell with the ghost flags of the last exchange, so
+        an edited cell next to a block face or a periodic face collides with
+        its stale flag in its neighbours' ghost layer until freeze(); here
+        its images follow its current flag."""
         blocks = self.forest.local_blocks()
         if not any(b.data[self.flags_key].touched for b in blocks):
-            return
-        if not np.array_equal(self._dense_flags(), self._flag_snapshot):
-            raise ValidationError("flags were edited after BoundaryHandling.freeze(); call "
-                                  "freeze() again before the next sweep")
+            return self._sweep_masks
+        dense = self._dense_flags()
         for b in blocks:
             b.data[self.flags_key].touched = False
+        if np.array_equal(dense, self._sweep_flags):
+            return self._sweep_masks
+        self._sweep_masks = self._refresh(dense)
+        self._sweep_flags = dense
+        return self._sweep_masks
+
+    def _refresh(self, dense) -> Masks:
+        import torch
+        frozen = self.masks
+        if np.array_equal(dense, self._flag_snapshot):
+            return frozen
+        box = RankBox(self.forest)
+        g = _lib.Grid()
+        g.q, g.real_bytes = self.stencil.q, 8
+        g.nx, g.ny, g.nz = box.nx, box.ny, box.nz
+        g.xoff, g.pitch = 1, box.nx + 2
+        g.wrap_x, g.wrap_y = int(box.wrap_x), int(box.wrap_y)
+        g.zface_lo, g.zface_hi = box.zface_lo, box.zface_hi
+        dev = frozen.cellmask.device
+        tf = torch.from_numpy(dense[0].view(np.int32)).to(dev)
+        cm = torch.empty_like(frozen.cellmask)
+        big = np.iinfo(np.int32).max
+        err = torch.tensor([big], dtype=torch.int32, device=dev)
+        registry = box.blocks[0].data[self.flags_key].registry
+        _lib.call("lbm_refresh_fluid_mask", ctypes.byref(g), _lib.ptr(tf), _flag_bits(registry),
+                  _lib.ptr(frozen.cellmask), _lib.ptr(cm), _lib.ptr(err),
+                  _lib.stream_ptr(torch.cuda.current_stream(dev)))
+        e = int(err.item())
+        unflagged = None
+        if e != big:
+            c = e - 1
+            unflagged = (box.lo[0] + c % box.nx, box.lo[1] + (c // box.nx) % box.ny,
+                         box.lo[2] + c // (box.nx * box.ny))
+        return Masks(cm, frozen.typemask, frozen.counts, unflagged)
 
     def apply(self, block, src, dst) -> None:
         raise ValidationError("boundary links are fused into the stream-collide kernel on the "

@@ -3,8 +3,10 @@
 Replaces the reference's simulated runtime (SimRuntime / RankContext,
 pkg/src/blocksim/runtime/core.py:56-121,124-218) for the calls the LBM path
 makes: `rank`, `n_ranks`, `all_gather`, `all_reduce`, `barrier`.  The
-per-step halo traffic does not go through this object's Python API; it is a
-zero-copy NCCL send/recv of field slices (see halo.py).
+per-step halo traffic does not go through this object's Python API: the
+boundary-plane kernel stores the crossing directions into the neighbour's
+ghost plane (peer stores over NVLink, halo.PeerHalo), with NCCL send/recv of
+the contiguous runs as the fallback (halo.py).
 """
 from __future__ import annotations
 

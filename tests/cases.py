@@ -76,6 +76,18 @@ CASES = {
                                  model=("SRT_field", 21, 0.7, 1.9),
                                  force=("Guo", (1e-4, -3e-5, 2e-5)), init=("random", 21),
                                  steps=12, snapshots=(1, 12), layout="zyxf"),
+    # flags edited between sweeps WITHOUT a new freeze(): the reference keeps
+    # its frozen links and collides with the current flags (lbm/sweep.py:
+    # 107-108, 124-136) - a Fluid cell turned NoSlip and back, an obstacle
+    # core cell turned Fluid (cells away from block / periodic faces)
+    "d3q19_flag_edits": dict(stencil="D3Q19", dims=(12, 10, 12), root_dims=(1, 1, 1),
+                             periodic=(True, True, True),
+                             geometry=dict(kind="box_obstacle", lo=(4, 3, 5), hi=(7, 6, 8)),
+                             model=("TRT_magic", 1.6), force=("Guo", (1e-4, 2e-5, 0.0)),
+                             init=("random", 31), steps=12, snapshots=(4, 5, 8, 12),
+                             edits={4: ((2, 2, 2, "NoSlip"), (5, 4, 6, "Fluid")),
+                                    8: ((9, 7, 3, "NoSlip"), (2, 2, 2, "Fluid"))},
+                             layout="fzyx"),
     # Pressure anti-bounce-back (f1 row): D2Q9 box, pressure top row
     "d2q9_pressure_box": dict(stencil="D2Q9", dims=(8, 8, 1), root_dims=(1, 1, 1),
                               periodic=(False, False, False), geometry=dict(kind="pressure_box"),
@@ -249,12 +261,15 @@ def run_case(api, ctx, spec, *, pdf_kwargs=None):
     d = 2 if spec["stencil"] == "D2Q9" else 3
     out = {"pdf": {}, "macro": None, "links": None}
     snaps = set(spec["snapshots"])
+    edits = spec.get("edits", {})
     for s in range(1, spec["steps"] + 1):
         api.stream_collide(pdf, model, force=force, handling=handling)
         if s in snaps:
             g = api.gather_slice(forest, "pdf", (0, 0, 0), forest.global_cells(0))
             if g is not None:
                 out["pdf"][s] = g
+        for (x, y, z, name) in edits.get(s, ()):
+            _edit_flag(api, forest, x, y, z, name)
     if spec.get("macro"):
         forest.register_data("rho", api.FieldDataHandler(nf=1, ghost_layers=0))
         forest.register_data("vel", api.FieldDataHandler(nf=d, ghost_layers=0))
@@ -271,6 +286,16 @@ def run_case(api, ctx, spec, *, pdf_kwargs=None):
         tot = ctx.all_gather(counts)
         out["links"] = {n: sum(tot[r][n] for r in tot) for n in counts}
     return out if ctx.rank == 0 else None
+
+
+def _edit_flag(api, forest, x, y, z, name):
+    """Set global interior cell (x, y, z) to flag `name` on the owning
+    block, without a new BoundaryHandling.freeze()."""
+    for block in forest.local_blocks():
+        lo, hi = forest.cell_box(block.id)
+        if lo[0] <= x < hi[0] and lo[1] <= y < hi[1] and lo[2] <= z < hi[2]:
+            ff = block.data["flags"]
+            ff.interior[z - lo[2], y - lo[1], x - lo[0]] = ff.registry[name]
 
 
 def setup_case(api, ctx, spec, *, pdf_kwargs=None):
@@ -481,10 +506,14 @@ def oracle_run(spec, oracle):
     dom.set_full(pdf)
     out = {}
     done = 0
-    for s in sorted(spec["snapshots"]):
+    edits = spec.get("edits", {})
+    for s in sorted(set(spec["snapshots"]) | set(edits)):
         dom.run(s - done)
         done = s
-        out[s] = dom.rform()
+        if s in spec["snapshots"]:
+            out[s] = dom.rform()
+        for (x, y, z, name) in edits.get(s, ()):
+            dom.edit_flag(x, y, z, name)
     return {"pdf": out, "domain": dom}
 
 

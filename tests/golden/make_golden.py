@@ -123,6 +123,110 @@ def make_coupling():
     (HERE / "digests.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
 
 
+SLOT_DIMS = (7, 5, 6)   # x, y, z of the slot box, ghost ring included
+
+
+def slot_cases():
+    """(name, stencil name, model kind, force, omega_window?, fluid bits,
+    view layout) of the kernel-slot goldens (make_slot)."""
+    out = []
+    forces = {"none": None, "guo": ("Guo", (3e-4, -2e-4, 1e-4)), "guox": ("Guo", (1e-4, 0.0, 0.0))}
+    for sname, models in (("D2Q9", ("srt", "trt", "mrt")),
+                          ("D3Q19", ("srt", "trt", "trtmagic", "mrt")),
+                          ("D3Q27", ("srt", "trt", "rawmrt"))):
+        for m in models:
+            for fname in forces:
+                lay = "soa" if (len(out) % 2) else "aos"
+                out.append((f"{sname}_{m}_{fname}", sname, m, fname, False, 1, lay))
+        out.append((f"{sname}_srt_shift", sname, "srt", "shift", False, 1, "aos"))
+        out.append((f"{sname}_srt_window_guo", sname, "srt", "guo", True, 1, "soa"))
+    out.append(("D3Q19_trt_multibit", "D3Q19", "trt", "none", False, 1 | 8, "soa"))
+    return out
+
+
+def make_slot():
+    """Kernel slot: the reference's own impl.collide and
+    impl.stream_pull (_kernels/_core_py.py:70-218) on a flagged box with its
+    ghost ring, for every model / force / view layout the slot accepts."""
+    import blocksim.lbm as L
+    from blocksim._kernels import _core_py as impl
+    from blocksim.lbm.collision import _kernel_params
+    import oracle
+    rng = np.random.default_rng(77)
+    X, Y, Z = SLOT_DIMS
+    out = {}
+    stencils = {"D2Q9": L.D2Q9, "D3Q19": L.D3Q19, "D3Q27": L.D3Q27}
+    for name, sname, m, fname, window, bits, lay in slot_cases():
+        st = stencils[sname]
+        q = st.q
+        rho = rng.uniform(0.8, 1.2, (Z, Y, X))
+        u = rng.uniform(-0.08, 0.08, (Z, Y, X, 3))
+        if st.d == 2:
+            u[..., 2] = 0.0
+        f = L.equilibrium(rho, u, st) * (1.0 + 0.03 * rng.uniform(-1, 1, (Z, Y, X, q)))
+        flags = rng.choice(np.array([0, 1, 2, 4, 8, 9, 16], dtype=np.uint32), size=(Z, Y, X))
+        if m == "srt":
+            model = L.SRT(1.3)
+        elif m == "trt":
+            model = L.TRT(1.3, 0.9)
+        elif m == "trtmagic":
+            model = L.TRT.with_magic(1.7)
+        elif m == "mrt":
+            rates = [1.0] * q
+            rates[q // 2:] = [1.4] * (q - q // 2)
+            model = L.MRT(st, rates)
+        else:   # D3Q27 raw-moment MRT through the generic branch (SURVEY 8c)
+            model = None
+        force = None
+        if fname in ("guo", "guox"):
+            force = L.Guo({"guo": (3e-4, -2e-4, 1e-4), "guox": (1e-4, 0.0, 0.0)}[fname])
+        elif fname == "shift":
+            force = L.SimpleShift((3e-4, -2e-4, 1e-4))
+        if model is None:
+            params = _kernel_params(st, L.SRT(1.0), force)
+            del params["omega"]
+            M = oracle.raw_moment_basis_d3q27(oracle.STENCILS["D3Q27"])
+            S = np.full(q, 1.0)
+            S[4:9] = 1.9
+            params["M"], params["Minv"], params["S"] = M, np.linalg.inv(M), S
+            if force is not None:
+                params["guo_matrix"] = params["Minv"] @ (np.eye(q) - 0.5 * np.diag(S)) @ M
+            mode = 2
+        else:
+            params = _kernel_params(st, model, force)
+            mode = model.mode
+        if window:
+            params["omega_window"] = rng.uniform(0.7, 1.9, (Z, Y, X))
+        if lay == "soa":
+            raw = np.ascontiguousarray(np.moveaxis(f, 3, 0))
+            view = np.moveaxis(raw, 0, 3)
+        else:
+            view = f.copy()
+        impl.collide(view, flags, np.uint32(bits), mode, params)
+        out[f"{name}__in"] = f
+        out[f"{name}__flags"] = flags
+        out[f"{name}__out"] = np.ascontiguousarray(view)
+        if window:
+            out[f"{name}__window"] = params["omega_window"]
+        # the params dict itself, as plain arrays (keys with a scalar / array value)
+        for k, v in params.items():
+            if v is None:
+                continue
+            out[f"{name}__p_{k}"] = np.asarray(v)
+        out[f"{name}__mode"] = np.asarray(mode)
+        out[f"{name}__bits"] = np.asarray(bits, dtype=np.uint32)
+        out[f"{name}__layout"] = np.asarray(lay)
+    for sname, st in stencils.items():
+        q = st.q
+        src = rng.standard_normal((Z, Y, X, q))
+        dst = rng.standard_normal((Z, Y, X, q))
+        out[f"pull_{sname}__src"], out[f"pull_{sname}__dst"] = src, dst.copy()
+        impl.stream_pull(src, dst, st.cx, st.cy, st.cz, 1)
+        out[f"pull_{sname}__out"] = dst
+    np.savez(HERE / "slot.npz", **out)
+    print("slot:", len(slot_cases()), "collide cases")
+
+
 def make_units():
     """Reference unit functions on seeded random cells."""
     import blocksim.lbm as L
@@ -174,6 +278,8 @@ if __name__ == "__main__":
     args = sys.argv[1:]
     if args == ["snapshot"]:
         make_snapshot()
+    elif args == ["slot"]:
+        make_slot()
     elif args == ["coupling"]:
         make_coupling()
     else:
@@ -181,3 +287,4 @@ if __name__ == "__main__":
         if not args:
             make_snapshot()
             make_coupling()
+            make_slot()

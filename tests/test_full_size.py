@@ -1,0 +1,197 @@
+"""Full-size parity of the configurations bench.py times.
+
+The bench's own workload builder (bench.build / bench.init_state: same
+geometry, seeds, walls, models and kernel code path, including the fp64
+keep-in-L2 link hint that switches on for 512^2 planes) runs on the GPU;
+the C oracle (oracle/lbm_oracle.c, pinned bit for bit to the reference's
+goldens) runs the same inputs on the host cores.  Reference path matched:
+/root/reference/pkg/src/blocksim/lbm/sweep.py:93-151.
+
+* config 4 fp64 (512^3, 20 % sphere tile, z walls, TRT magic 1.8 + Guo)
+  and config 3 (512^3 periodic, random rho/u): 20 steps, BITWISE on the
+  full interior;
+* config 1 (128^3 porous): all 1000 steps, bitwise;
+* config 4 fp32 (512^3 x 200) and config 2 fp32 (256^3 x 500): within the
+  BASELINE 1e-5 relative tolerance of the GPU's fp64 run of the same
+  workload (that fp64 path is itself bitwise to the oracle, above and in
+  test_gpu_parity.py); the measured error is printed;
+* the keep-in-L2 path (LBM_B200_LINK_HINT=1) on a small grid, bitwise.
+
+Host RAM: the 512^3 oracle holds two 20.6 GB fields (the GPU box has
+~196 GB); comparisons stream the GPU's readout in z-chunks.
+"""
+import os
+import time
+
+import numpy as np
+import pytest
+
+import cases
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32_REL = 1e-5   # BASELINE.json: fp32 relative tolerance
+
+
+def _bench():
+    import bench
+    return bench
+
+
+def _gpu_run(config, dtype, steps):
+    """Build the bench workload, run `steps` sweeps, return the device
+    R-form (q, nz, ny, nx) fp64 and the dims."""
+    import torch
+    import paper_1909_13772_b200 as P
+    bench = _bench()
+    cfg = bench.CONFIGS[config]
+    ctx = P.Context()
+    forest, pdf, handling, model, force, dims = bench.build(cfg, ctx, dtype, P)
+    bench.init_state(cfg, pdf, dims, ctx, P)
+    P.stream_collide_n(pdf, model, steps, force=force, handling=handling)
+    kind, out = pdf.lattice.readout_device()
+    assert kind == "interior"
+    torch.cuda.synchronize()
+    del forest, pdf, handling
+    return out, dims
+
+
+def _oracle_domain(config, dims):
+    """The same workload as bench.build / init_state, on the C oracle."""
+    bench = _bench()
+    from paper_1909_13772_b200 import workloads
+    cfg = bench.CONFIGS[config]
+    st = oracle.STENCILS[cfg["stencil"]]
+    nx, ny, nz = dims
+    X, Y, Z = nx + 2, ny + 2, nz + 2
+    bits = {"Fluid": 1, "NoSlip": 2, "UBB": 4, "Pressure": 8, "Solid": 16}
+    flags = None
+    geo = cfg["geometry"]
+    if geo is not None:
+        if geo == "tiles":
+            code = workloads.sphere_mask((nx, ny, nz), 100, 4.0, 8.0, 0.20,
+                                         (True, True, False)).astype(np.int8)
+            code[0] = code[-1] = 1           # global z-min / z-max walls (one tile)
+        elif geo == "spheres25":
+            code = workloads.porous_channel_flags((nx, ny, nz), 1, 0.25).astype(np.int8)
+        else:
+            code = workloads.cavity_flags((nx, ny, nz))
+        flags = np.zeros((Z, Y, X), dtype=np.uint32)
+        inner = np.full(code.shape, bits["Fluid"], dtype=np.uint32)
+        inner[code == 1] = bits["NoSlip"]
+        inner[code == 2] = bits["UBB"]
+        flags[1:-1, 1:-1, 1:-1] = inner
+        del code, inner
+    m = cfg["model"]
+    force = (cfg["force"], 0.0, 0.0) if cfg["force"] else None
+    if m[0] == "TRT_magic":
+        we, wo = oracle.trt_magic(m[1])
+        model = oracle.Model("TRT", omega_e=we, omega_o=wo, force=force)
+    elif m[0] == "SRT":
+        model = oracle.Model("SRT", omega=m[1], force=force)
+    else:
+        raise AssertionError(m)
+    dom = oracle.Domain(st, dims, cfg["periodic"], model, flags, bits,
+                        ubb_velocity=cfg.get("ubb", (0.0, 0.0, 0.0)))
+    del flags
+    for i in range(st.q):
+        dom.a[i] = st.w[i]                   # fill_equilibrium(pdf): rho 1, u 0 everywhere
+    if cfg["init"] == "random":
+        rho, u = workloads.random_rho_u(dims, 1000)   # bench.init_state, rank 0
+        for z0 in range(0, nz, 64):
+            sl = slice(z0, min(nz, z0 + 64))
+            feq = oracle.equilibrium(rho[sl], u[sl], st)
+            dom.a[:, 1 + sl.start:1 + sl.stop, 1:-1, 1:-1] = np.moveaxis(feq, 3, 0)
+        del rho, u
+    dom.b[...] = dom.a
+    return dom
+
+
+def _compare_bitwise(out, dom, chunk=32):
+    q, nz = out.shape[0], out.shape[1]
+    worst = 0.0
+    equal = True
+    for z0 in range(0, nz, chunk):
+        z1 = min(nz, z0 + chunk)
+        g = out[:, z0:z1].cpu().numpy()
+        o = dom.a[:, 1 + z0:1 + z1, 1:-1, 1:-1]
+        if not np.array_equal(g, o):
+            equal = False
+            worst = max(worst, float(np.abs(g - o).max()))
+    return equal, worst
+
+
+def _rel_err(a, b, chunk=16):
+    """max |a - b| / |b| over device tensors (q, nz, ny, nx), in z-chunks."""
+    worst = 0.0
+    for z0 in range(0, a.shape[1], chunk):
+        x, y = a[:, z0:z0 + chunk], b[:, z0:z0 + chunk]
+        worst = max(worst, float(((x - y).abs() / y.abs()).max().item()))
+    return worst
+
+
+@pytest.mark.parametrize("config", ["c4", "c3"])
+def test_512cubed_fp64_bitwise_vs_oracle(config):
+    """BASELINE configs 4 and 3 at their bench size (512^3), 20 steps."""
+    import torch
+    steps = 20
+    t0 = time.perf_counter()
+    out, dims = _gpu_run(config, "f64", steps)
+    t1 = time.perf_counter()
+    dom = _oracle_domain(config, dims)
+    dom.run(steps)
+    t2 = time.perf_counter()
+    equal, worst = _compare_bitwise(out, dom)
+    print(f"{config} 512^3 x {steps}: gpu {t1 - t0:.1f} s, oracle {t2 - t1:.1f} s, "
+          f"bitwise={equal} max|d|={worst:.3e}")
+    del dom, out
+    torch.cuda.empty_cache()
+    assert equal, f"{config}: GPU != oracle, max|d| = {worst:.3e} (tol 1e-12)"
+
+
+def test_config1_all_1000_steps_bitwise():
+    """BASELINE config 1 (128^3 porous, TRT magic 1.7 + Guo 1e-6) for its
+    full 1000 steps, bitwise on the full interior."""
+    out, dims = _gpu_run("c1", "f64", 1000)
+    dom = _oracle_domain("c1", dims)
+    dom.run(1000)
+    equal, worst = _compare_bitwise(out, dom)
+    assert equal, f"config 1 x 1000: max|d| = {worst:.3e}"
+
+
+def test_config4_fp32_512cubed_200_steps_within_1e5():
+    import torch
+    ref, _ = _gpu_run("c4", "f64", 200)
+    got, _ = _gpu_run("c4", "f32", 200)
+    rel = _rel_err(got, ref)
+    print(f"config 4 fp32 512^3 x 200: max rel err vs fp64 = {rel:.3e}")
+    del ref, got
+    torch.cuda.empty_cache()
+    assert rel < TOL_F32_REL, rel
+
+
+def test_config2_fp32_256cubed_500_steps_within_1e5():
+    """D3Q27 raw-moment MRT cavity: fp32 (factorised MRT, fp32 registers)
+    against the fp64 dense-MRT run (bitwise to the oracle at 48^3 in
+    test_gpu_parity.py) of the same 256^3 x 500 workload."""
+    import torch
+    ref, _ = _gpu_run("c2", "f64", 500)
+    got, _ = _gpu_run("c2", "f32", 500)
+    rel = _rel_err(got, ref)
+    print(f"config 2 fp32 256^3 x 500: max rel err vs fp64 = {rel:.3e}")
+    del ref, got
+    torch.cuda.empty_cache()
+    assert rel < TOL_F32_REL, rel
+
+
+def test_link_hint_path_bitwise_small(monkeypatch):
+    """The evict_last link-hint loads (on by default only for >= 16 MB
+    planes) forced on a 24^3 porous case: bitwise vs the oracle."""
+    monkeypatch.setenv("LBM_B200_LINK_HINT", "1")
+    import paper_1909_13772_b200 as P
+    spec = dict(cases.DIGEST_CASES["c1_trt_guo_porous_24"])
+    spec.update(snapshots=(50,))
+    res = cases.run_case(cases.b200_api(), P.Context(), spec)
+    ores = cases.oracle_run(spec, oracle)
+    assert res["pdf"][50].tobytes() == ores["pdf"][50].tobytes()

@@ -150,7 +150,8 @@ def test_config2_model_fp64_bitwise(api):
 
 @pytest.mark.parametrize("spec_name", ["c0", "c1", "c2"])
 def test_fp32_storage_within_1e5_relative(api, spec_name):
-    """fp32 PDFs (stored as f - w_i, fp64 arithmetic) vs the fp64 oracle."""
+    """fp32 PDFs (stored as f - w_i, fp32 arithmetic on the centred populations)
+    vs the fp64 oracle."""
     specs = {
         "c0": dict(stencil="D3Q19", dims=(48, 48, 48), root_dims=(1, 1, 1),
                    periodic=(True, True, True), geometry=None, model=("TRT_magic", 1.8),
@@ -580,3 +581,84 @@ def test_fused_peer_halo_setup_failure_falls_back_collectively(api, monkeypatch)
         assert kinds == ["staged"] and fell_back
     base = cases.run_case(api, _ctx(), spec)
     assert per_rank[0][0]["pdf"][12].tobytes() == base["pdf"][12].tobytes()
+
+
+# ------------------------------------------- parameter identity
+def _random_lattice(P, dims, seed, stencil="D3Q19"):
+    ctx = _ctx()
+    nx, ny, nz = dims
+    forest = P.create_forest(ctx, (0, 0, 0, 1, 1, 1), (1, 1, 1), periodic=(True, True, True),
+                             cells_per_block=(nx, ny, nz))
+    st = getattr(P, stencil)
+    pdf = P.PdfField(forest, st, layout="fzyx")
+    P.fill_equilibrium(pdf)
+    rho, u = cases.workloads.random_rho_u(dims, seed)
+    blk = forest.local_blocks()[0]
+    pdf.src(blk).interior[...] = P.equilibrium(rho, u, st)
+    return forest, pdf, blk
+
+
+def _oracle_random(dims, seed, model, steps):
+    st = oracle.STENCILS["D3Q19"]
+    spec = dict(stencil="D3Q19", dims=dims, root_dims=(1, 1, 1), periodic=(True, True, True),
+                geometry=None, init=("random", seed))
+    full, _, _ = cases.oracle_inputs(spec, oracle)
+    d = oracle.Domain(st, dims, (True, True, True), model)
+    d.set_full(full)
+    d.run(steps)
+    return d
+
+
+def test_mrt_tables_of_two_lattices_across_graph_replays(api):
+    """Two MRT lattices with different rates on one device, each advanced
+    through stream_collide_n (captured two-step graphs): the constant-memory
+    tables a replay reads are re-bound to its own model (lbm_bind_params)."""
+    import paper_1909_13772_b200 as P
+    dims = (12, 10, 8)
+    ra = [1.0] * 19
+    ra[9:16] = [1.4] * 7
+    rb = [1.2] * 19
+    rb[9:16] = [1.8] * 7
+    _, pa, ba = _random_lattice(P, dims, 41)
+    _, pb, bb = _random_lattice(P, dims, 42)
+    ma, mb = P.MRT(P.D3Q19, ra), P.MRT(P.D3Q19, rb)
+    force = P.Guo((1e-4, 0.0, -2e-5))
+    P.stream_collide_n(pa, ma, 6, force=force)
+    P.stream_collide_n(pb, mb, 6, force=force)
+    P.stream_collide_n(pa, ma, 6, force=force)
+    st = oracle.STENCILS["D3Q19"]
+    M = oracle.moment_basis(st)
+    for pdf, blk, rates, seed, steps in ((pa, ba, ra, 41, 12), (pb, bb, rb, 42, 6)):
+        model = oracle.Model("MRT", M=M.astype(np.float64), Minv=oracle.basis_inverse(M),
+                             S=np.array(rates), force=(1e-4, 0.0, -2e-5))
+        want = _oracle_random(dims, seed, model, steps).rform()
+        assert pdf.src(blk).interior.tobytes() == want.tobytes(), rates
+
+
+def test_mutated_model_and_wall_velocity_take_effect(api):
+    """Parameters are keyed by value, not object identity: a lid velocity
+    ramped on the same BoundaryHandling and a rate changed on the same SRT
+    object apply to the next sweep, as in the reference (boundary.py:165-171,
+    sweep.py:116)."""
+    import paper_1909_13772_b200 as P
+    spec = dict(stencil="D3Q19", dims=(10, 8, 9), root_dims=(1, 1, 1),
+                periodic=(False, False, False), geometry=dict(kind="cavity"),
+                model=("SRT", 1.5), force=None, init=("rest",),
+                ubb_velocity=(0.05, 0.0, 0.0), layout="fzyx")
+    forest, pdf, handling, model, force, st = cases.setup_case(cases.b200_api(), _ctx(), spec)
+    phases = (((0.05, 0.0, 0.0), 1.5), ((0.08, 0.01, 0.0), 1.5), ((0.08, 0.01, 0.0), 1.1))
+    for uw, om in phases:
+        handling.ubb_velocity = uw
+        model.omega = om
+        for _ in range(3):
+            P.stream_collide(pdf, model, handling=handling)
+    got = pdf.src(forest.local_blocks()[0]).interior.copy()
+    full, flags, bits = cases.oracle_inputs(spec, oracle)
+    ost = oracle.STENCILS["D3Q19"]
+    for uw, om in phases:
+        d = oracle.Domain(ost, spec["dims"], spec["periodic"], oracle.Model("SRT", omega=om),
+                          flags, bits, ubb_velocity=uw)
+        d.set_full(full)
+        d.run(3)
+        full = d.a.copy()
+    assert got.tobytes() == d.rform().tobytes()
