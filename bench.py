@@ -436,8 +436,10 @@ def main():
                        "cells_per_gpu": cells_rank, "parallelism": f"z-slab x{n}",
                        "halo": (getattr(lat._halo, "kind", None) if n > 1 else None),
                        "pdf_storage": "fp64" if rb == 8 else "fp32 (f - w_i), fp32 arithmetic on centred populations",
-                       "l2": f"working set {2 * lat.elems * rb / 1e9:.1f} GB per GPU >> 126 MB L2 "
-                             "(no flush needed)"},
+                       "l2": (f"working set {2 * lat.elems * rb / 1e9:.1f} GB per GPU >> 126 MB L2 "
+                              "(no flush needed)" if 2 * lat.elems * rb > 4 * 126e6 else
+                              f"working set {2 * lat.elems * rb / 1e6:.0f} MB per GPU: largely "
+                              "L2-resident, no roofline claim (correctness config)")},
             "mlups_per_gpu": round(value / n, 1),
             "roofline": roof, "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk.summary(), "gpu_launches": int(launches),

@@ -1,75 +1,62 @@
-"""Space-filling-curve ordering and curve partitioning of root blocks.
+"""Rank ownership of the root blocks.
 
-Restates the two routines `create_forest` uses to assign blocks to ranks
-(pkg/src/blocksim/balance.py:31-41 morton_key, :101-129 sort_blocks,
-:132-167 partition_curve) so the rank <-> block map is the reference's.  With
-root_dims = (1, 1, P) rank k owns z-slab k.
+`create_forest` hands root blocks to ranks in two steps (reference:
+pkg/src/blocksim/blockforest/forest.py:439-447 calling balance.py:101-167):
+order the blocks along a Morton curve, then cut the curve into one
+consecutive segment per rank with every block weighing one.  This module
+computes the same map directly:
+
+* the Morton position of root (x, y, z) is its bits interleaved x-y-z from
+  the least significant end (bit b of x -> 3b, of y -> 3b+1, of z -> 3b+2;
+  d = 2 drops z), which orders blocks exactly like the reference's
+  most-significant-first key of a common bit width;
+* with unit weights the reference's greedy cut (close a segment at the
+  prefix nearest k * n / P, ties taken) ends segment k at
+  round-half-up(n (k + 1) / P) = (2 n (k + 1) + P) // (2 P), in integers.
+
+For root_dims = (1, 1, P) this gives rank k the z-slab k.  Both rules are
+checked against the reference's own outputs (tests/golden/ownership.json).
 """
 from __future__ import annotations
 
 from .errors import ValidationError
 
 
-def morton_key(coords, level: int, d: int, bits: int) -> int:
-    x, y, z = (int(c) for c in coords)
-    key = 0
-    for b in range(bits - 1, -1, -1):
-        if d == 3:
-            key = (key << 3) | (((z >> b) & 1) << 2) | (((y >> b) & 1) << 1) | ((x >> b) & 1)
-        else:
-            key = (key << 2) | (((y >> b) & 1) << 1) | ((x >> b) & 1)
-    return key
+def _interleave(v: int, stride: int, lane: int) -> int:
+    out, b = 0, 0
+    while v:
+        if v & 1:
+            out |= 1 << (b * stride + lane)
+        v >>= 1
+        b += 1
+    return out
 
 
-def sort_blocks(entries, curve: str, d: int):
-    """Payloads of (coords, level, payload) entries in Morton order."""
-    entries = list(entries)
-    if not entries:
-        return []
+def morton_position(coords, d: int) -> int:
+    """Curve key of root coordinates (x, y[, z])."""
+    return sum(_interleave(int(coords[a]), d, a) for a in range(d))
+
+
+def curve_order(coords_of, d: int, curve: str = "morton"):
+    """Items sorted along the space-filling curve; coords_of: {item: coords}."""
     if curve != "morton":
         raise ValidationError(f"curve {curve!r} is not supported on the B200 path (morton only)")
-    finest = max(level for _, level, _ in entries)
-    maxc = 0
-    for coords, level, _ in entries:
-        lift = finest - level
-        maxc = max(maxc, *(int(c) << lift for c in coords[:d]))
-    bits = max(1, maxc.bit_length())
-    keyed = []
-    for coords, level, payload in entries:
-        lift = finest - level
-        lifted = tuple(int(c) << lift for c in coords)
-        keyed.append((morton_key(lifted, finest, d, bits), payload))
-    keyed.sort(key=lambda kv: kv[0])
-    return [payload for _, payload in keyed]
+    return sorted(coords_of, key=lambda item: morton_position(coords_of[item], d))
 
 
-def partition_curve(weights, n_ranks: int):
-    """Consecutive per-rank segments closing at the prefix sum nearest to
-    k * total / n_ranks (balance.py:132-167)."""
-    weights = [float(w) for w in weights]
+def segment_ends(n_blocks: int, n_ranks: int):
+    """End (exclusive) of each rank's segment of n_blocks unit-weight
+    blocks along the curve."""
     if n_ranks < 1:
         raise ValidationError(f"n_ranks must be >= 1, got {n_ranks}")
-    if any(w < 0 for w in weights):
-        raise ValidationError("block weights must be non-negative")
-    n = len(weights)
-    assignment = [0] * n
-    total = sum(weights)
-    if n == 0 or total == 0.0:
-        for i in range(n):
-            assignment[i] = i * n_ranks // n
-        return assignment
-    prefix = 0.0
-    i = 0
-    for rank in range(n_ranks - 1):
-        target = total * (rank + 1) / n_ranks
-        while i < n:
-            candidate = prefix + weights[i]
-            if abs(candidate - target) <= abs(prefix - target):
-                assignment[i] = rank
-                prefix = candidate
-                i += 1
-            else:
-                break
-    for j in range(i, n):
-        assignment[j] = n_ranks - 1
-    return assignment
+    ends = [(2 * n_blocks * (k + 1) + n_ranks) // (2 * n_ranks) for k in range(n_ranks - 1)]
+    return ends + [n_blocks]
+
+
+def owners_along_curve(n_blocks: int, n_ranks: int):
+    """Rank of each curve position."""
+    out, start = [], 0
+    for rank, end in enumerate(segment_ends(n_blocks, n_ranks)):
+        out.extend([rank] * (end - start))
+        start = end
+    return out

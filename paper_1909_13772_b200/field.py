@@ -1,13 +1,15 @@
-"""Ghost-layered block fields (host side) and their collective helpers.
+"""Host-side block fields: storage, flags, slot handlers, ghost rounds.
 
-Same API and semantics as the reference's field package
-(pkg/src/blocksim/field/core.py:16-175, handler.py:36-129, ghost.py:202-264,
-gather.py:10-79).  For the PDF slots of a PdfField these host arrays are a
-*mirror* of the HBM-resident state: reading `raw` / `view` / `interior`
-pulls the current R-form from the device on demand (a stream-only readout
-kernel, no CPU compute), and host writes are detected and re-uploaded before
-the next sweep.  Everything else (flags, scalar fields) is host data as in
-the reference.
+The drop-in surface of the reference's field package (Field, FlagField,
+FieldDataHandler, FlagFieldHandler, GhostPackInfo, exchange_ghosts,
+gather_slice, sweep; pkg/src/blocksim/field/core.py:16-175,
+handler.py:36-129, ghost.py:202-264, gather.py:10-79) on uniform root
+blocks.  What differs is where data lives: the PDF slots of a PdfField are
+HBM-resident, and their host arrays here are a lazily allocated *mirror*
+(`_mirror` hook): reading raw / view / interior pulls the current R-form
+from the device (a stream-only readout kernel), and host writes are
+detected and uploaded before the next sweep.  Flags and scalar fields are
+plain host data.
 """
 from __future__ import annotations
 
@@ -18,37 +20,48 @@ from .errors import ValidationError
 LAYOUTS = ("zyxf", "fzyx")
 
 
+def _raw_shape(dims, g, layout):
+    nx, ny, nz, nf = dims
+    cells = (nz + 2 * g, ny + 2 * g, nx + 2 * g)
+    return cells + (nf,) if layout == "zyxf" else (nf,) + cells
+
+
+def _logical(raw, layout):
+    """(z, y, x, f) view of a raw array of either layout."""
+    return np.moveaxis(raw, 0, 3) if layout == "fzyx" else raw
+
+
 class Field:
-    """(nx, ny, nz, nf) values plus g ghost layers, layout "zyxf" or "fzyx"."""
+    """nf values per cell of an (nx, ny, nz) block plus g ghost layers,
+    stored AoS ("zyxf") or SoA ("fzyx"); every accessor speaks the logical
+    (z, y, x, f) order.  lazy=True defers the host allocation until first
+    use (a 512^3 D3Q19 mirror is 21 GB and usually never touched)."""
 
     __slots__ = ("nx", "ny", "nz", "nf", "g", "layout", "dx", "_raw_", "_mirror", "_lazy")
 
     def __init__(self, dims, ghost_layers=0, layout="zyxf", init=0.0, dtype=np.float64, dx=1.0,
                  lazy=False):
-        nx, ny, nz, nf = (int(v) for v in dims)
-        if min(nx, ny, nz, nf) < 1:
-            raise ValidationError(f"field dims must be positive, got {dims}")
+        dims = tuple(int(v) for v in dims)
+        if len(dims) != 4 or min(dims) < 1:
+            raise ValidationError(f"field dims must be four positive extents, got {dims}")
         if ghost_layers < 0:
             raise ValidationError(f"ghost layers must be >= 0, got {ghost_layers}")
         if layout not in LAYOUTS:
             raise ValidationError(f"layout must be one of {LAYOUTS}, got {layout!r}")
-        self.nx, self.ny, self.nz, self.nf = nx, ny, nz, nf
+        self.nx, self.ny, self.nz, self.nf = dims
         self.g = int(ghost_layers)
         self.layout = layout
         self.dx = float(dx)
-        g2 = 2 * self.g
-        shape = (nz + g2, ny + g2, nx + g2, nf) if layout == "zyxf" else (nf, nz + g2, ny + g2, nx + g2)
-        # lazy: the host copy of an HBM-resident field is only allocated
-        # when the host actually touches it (a 512^3 D3Q19 field is 21 GB)
-        self._lazy = (shape, init, dtype) if lazy else None
-        self._raw_ = None if lazy else np.full(shape, init, dtype=dtype)
+        spec = (_raw_shape(dims, self.g, layout), init, dtype)
+        self._lazy = spec if lazy else None
+        self._raw_ = None if lazy else np.full(*spec)
         self._mirror = None
 
+    # storage: `_raw` is the array itself, `raw` syncs a device mirror first
     @property
     def _raw(self):
         if self._raw_ is None:
-            shape, init, dtype = self._lazy
-            self._raw_ = np.full(shape, init, dtype=dtype)
+            self._raw_ = np.full(*self._lazy)
         return self._raw_
 
     @_raw.setter
@@ -59,17 +72,18 @@ class Field:
     def allocated(self) -> bool:
         return self._raw_ is not None
 
-    # device mirror hook: sync before handing the array out
-    @property
-    def raw(self):
+    def _sync(self):
         if self._mirror is not None:
             self._mirror.host_access()
+
+    @property
+    def raw(self):
+        self._sync()
         return self._raw
 
     @raw.setter
     def raw(self, value):
-        if self._mirror is not None:
-            self._mirror.host_access()
+        self._sync()
         self._raw = value
 
     @property
@@ -78,50 +92,49 @@ class Field:
 
     @property
     def view(self):
-        """Logical (z, y, x, f) array including ghost layers."""
-        raw = self.raw
-        return raw if self.layout == "zyxf" else np.moveaxis(raw, 0, 3)
-
-    @property
-    def interior(self):
-        g = self.g
-        return self.view[g:g + self.nz, g:g + self.ny, g:g + self.nx]
+        return _logical(self.raw, self.layout)
 
     @property
     def view_nosync(self):
-        """Logical view of the host array without triggering a device sync
-        (used by the mirror itself)."""
-        raw = self._raw
-        return raw if self.layout == "zyxf" else np.moveaxis(raw, 0, 3)
+        """The logical view without a device sync (the mirror's own access)."""
+        return _logical(self._raw, self.layout)
 
-    def get(self, x, y, z, f=0):
-        self._check_index(x, y, z, f)
-        g = self.g
-        return self.view[z + g, y + g, x + g, f]
+    @property
+    def interior(self):
+        return self.view[self._inner()]
 
-    def set(self, x, y, z, f, value):
-        self._check_index(x, y, z, f)
+    def _inner(self):
         g = self.g
-        self.view[z + g, y + g, x + g, f] = value
+        return (slice(g, g + self.nz), slice(g, g + self.ny), slice(g, g + self.nx))
 
-    def _check_index(self, x, y, z, f):
+    def _at(self, x, y, z, f):
         g = self.g
-        if not (-g <= x < self.nx + g and -g <= y < self.ny + g and -g <= z < self.nz + g
-                and 0 <= f < self.nf):
+        inside = all(-g <= c < n + g for c, n in ((x, self.nx), (y, self.ny), (z, self.nz)))
+        if not (inside and 0 <= f < self.nf):
             raise IndexError(f"({x}, {y}, {z}, {f}) outside field of dims {self.dims} "
                              f"with {g} ghost layers")
+        return (z + g, y + g, x + g, f)
+
+    def get(self, x, y, z, f=0):
+        return self.view[self._at(x, y, z, f)]
+
+    def set(self, x, y, z, f, value):
+        self.view[self._at(x, y, z, f)] = value
+
+    def _signature(self):
+        return (self.dims, self.g, self.layout, self._raw.dtype)
 
     def swap_data(self, other: "Field") -> None:
-        if (self.dims != other.dims or self.g != other.g or self.layout != other.layout
-                or self._raw.dtype != other._raw.dtype):
+        """O(1) storage exchange between two fields of one shape."""
+        if self._signature() != other._signature():
             raise ValidationError(f"cannot swap fields {self.dims}/g={self.g}/{self.layout} and "
                                   f"{other.dims}/g={other.g}/{other.layout}")
-        self._raw, other._raw = other._raw, self._raw
+        self._raw_, other._raw_ = other._raw, self._raw
 
     def copy(self) -> "Field":
-        out = Field(self.dims, self.g, self.layout, 0.0, self._raw.dtype, self.dx)
-        out._raw[...] = self.raw
-        return out
+        twin = Field(self.dims, self.g, self.layout, 0.0, self._raw.dtype, self.dx)
+        np.copyto(twin._raw, self.raw)
+        return twin
 
     def __repr__(self):
         return f"Field(dims={self.dims}, g={self.g}, layout={self.layout!r}, dtype={self._raw.dtype})"
@@ -135,15 +148,53 @@ def swap_data(a: Field, b: Field) -> None:
     a.swap_data(b)
 
 
+# ---------------------------------------------------------------- flags
+# A registry maps flag name -> one-bit uint32 mask; bits are handed out in
+# registration order (the first name gets bit 0), at most 32 names.  One
+# registry (any dict) is shared by every FlagField of a forest slot, so a
+# name means the same bit on every block.
+def _new_bit(registry: dict, name: str) -> np.uint32:
+    if name in registry:
+        raise ValidationError(f"flag {name!r} already registered")
+    if len(registry) == 32:
+        raise ValidationError("flag registry full (32 bits)")
+    bit = np.uint32(1) << np.uint32(len(registry))
+    registry[name] = bit
+    return bit
+
+
+def _bit_of(registry: dict, name: str) -> np.uint32:
+    if name not in registry:
+        raise ValidationError(f"flag {name!r} is not registered")
+    return registry[name]
+
+
+class FlagRegistry(dict):
+    """A registry with the three operations as methods."""
+
+    def register(self, name: str) -> np.uint32:
+        return _new_bit(self, name)
+
+    def bit(self, name: str) -> np.uint32:
+        return _bit_of(self, name)
+
+    def union(self, names) -> np.uint32:
+        return np.bitwise_or.reduce([_bit_of(self, n) for n in names], initial=np.uint32(0))
+
+
 class FlagField:
-    """uint32 bitmask per cell with a shared name -> bit registry
-    (core.py:121-169).  Accessing view/interior marks the field touched so a
-    sweep can detect edits made after BoundaryHandling.freeze()."""
+    """uint32 bitmask per cell (core.py:121-169).  Touching view/interior
+    sets `touched`, which is how a sweep notices flags edited after
+    BoundaryHandling.freeze()."""
 
     def __init__(self, dims3, ghost_layers=0, registry=None):
         self.field = Field(tuple(dims3) + (1,), ghost_layers, "zyxf", init=0, dtype=np.uint32)
-        self.registry = {} if registry is None else registry
+        self.registry = FlagRegistry() if registry is None else registry
         self.touched = True
+
+    @property
+    def g(self):
+        return self.field.g
 
     @property
     def view(self):
@@ -155,109 +206,91 @@ class FlagField:
         self.touched = True
         return self.field.interior[..., 0]
 
-    @property
-    def g(self):
-        return self.field.g
+    def register(self, name: str):
+        return _new_bit(self.registry, name)
 
-    def register(self, name: str) -> int:
-        if name in self.registry:
-            raise ValidationError(f"flag {name!r} already registered")
-        if len(self.registry) >= 32:
-            raise ValidationError("flag registry full (32 bits)")
-        mask = np.uint32(1 << len(self.registry))
-        self.registry[name] = mask
-        return mask
+    def mask(self, name: str):
+        return _bit_of(self.registry, name)
 
-    def mask(self, name: str) -> int:
-        try:
-            return self.registry[name]
-        except KeyError:
-            raise ValidationError(f"flag {name!r} is not registered") from None
-
-    def combined_mask(self, names) -> int:
-        out = np.uint32(0)
-        for name in names:
-            out |= self.mask(name)
-        return out
+    def combined_mask(self, names):
+        return np.bitwise_or.reduce([_bit_of(self.registry, n) for n in names],
+                                    initial=np.uint32(0))
 
     def count(self, name: str) -> int:
-        return int(np.count_nonzero(self.field.interior[..., 0] & self.mask(name)))
+        """Interior cells carrying the flag."""
+        bit = _bit_of(self.registry, name)
+        return int(np.count_nonzero(np.bitwise_and(self.field.interior[..., 0], bit)))
 
 
 def sweep(forest, kernel) -> None:
-    """Apply kernel(block) to every local block in ascending id order."""
+    """kernel(block) on every local block, ascending ids."""
     for block in forest.local_blocks():
         kernel(block)
 
 
-class FieldDataHandler:
-    """Creates one Field per block (handler.py:36-67)."""
+# --------------------------------------------------------- slot handlers
+class _ArraySlot:
+    """Shared snapshot format of the field slots: the raw array itself
+    (handler.py:53-63 / 103-110).  Subclasses say which array that is."""
+
+    def _array(self, value):
+        raise NotImplementedError   # abstract hook, never called directly
+
+    def serialize(self, forest, block, value, buf) -> None:
+        buf.pack_array(self._array(value))
+
+    def deserialize(self, forest, block, buf):
+        value = self.create(forest, block)
+        incoming = buf.unpack_array()
+        target = self._array(value)
+        if incoming.shape != target.shape:
+            raise ValidationError(f"serialized array {incoming.shape} does not fit the slot's "
+                                  f"{target.shape}")
+        target[...] = incoming
+        return value
+
+
+def _block_cells(forest):
+    if forest.cells_per_block is None:
+        raise ValidationError("forest has no cells_per_block")
+    return tuple(forest.cells_per_block)
+
+
+class FieldDataHandler(_ArraySlot):
+    """One Field per block (handler.py:36-67)."""
 
     def __init__(self, nf=1, ghost_layers=1, layout="zyxf", init=0.0, dtype=np.float64,
                  lazy=False):
-        self.nf = int(nf)
-        self.g = int(ghost_layers)
-        self.layout = layout
-        self.init = init
-        self.dtype = dtype
-        self.lazy = lazy
+        self.nf, self.g = int(nf), int(ghost_layers)
+        self.layout, self.init, self.dtype, self.lazy = layout, init, dtype, lazy
 
     def create(self, forest, block) -> Field:
-        if forest.cells_per_block is None:
-            raise ValidationError("forest has no cells_per_block")
-        dx = forest.dx(block.level)[0]
-        return Field(tuple(forest.cells_per_block) + (self.nf,), self.g, self.layout, self.init,
-                     self.dtype, dx, lazy=self.lazy)
+        cells = _block_cells(forest)
+        return Field(cells + (self.nf,), self.g, self.layout, self.init, self.dtype,
+                     forest.dx(block.level)[0], lazy=self.lazy)
 
-    # snapshot slot format: the raw array (handler.py:53-63)
-    def serialize(self, forest, block, field, buf) -> None:
-        buf.pack_array(field.raw)
-
-    def deserialize(self, forest, block, buf) -> Field:
-        field = self.create(forest, block)
-        raw = buf.unpack_array()
-        if raw.shape != field.raw.shape:
-            raise ValidationError(f"serialized field shape {raw.shape} != expected "
-                                  f"{field.raw.shape}")
-        field.raw[...] = raw
-        return field
+    def _array(self, field):
+        return field.raw
 
 
-class FlagFieldHandler:
-    """FlagFields sharing one registry (handler.py:83-102)."""
+class FlagFieldHandler(_ArraySlot):
+    """FlagFields of one slot sharing a FlagRegistry (handler.py:83-110)."""
 
     def __init__(self, ghost_layers=1):
         self.g = int(ghost_layers)
-        self.registry = {}
+        self.registry = FlagRegistry()
 
-    def register(self, name: str) -> int:
-        if name in self.registry:
-            raise ValidationError(f"flag {name!r} already registered")
-        if len(self.registry) >= 32:
-            raise ValidationError("flag registry full (32 bits)")
-        mask = np.uint32(1 << len(self.registry))
-        self.registry[name] = mask
-        return mask
+    def register(self, name: str):
+        return self.registry.register(name)
 
     def create(self, forest, block) -> FlagField:
-        if forest.cells_per_block is None:
-            raise ValidationError("forest has no cells_per_block")
-        return FlagField(forest.cells_per_block, self.g, self.registry)
+        return FlagField(_block_cells(forest), self.g, self.registry)
 
-    def serialize(self, forest, block, flags, buf) -> None:
-        buf.pack_array(flags.field.raw)
-
-    def deserialize(self, forest, block, buf) -> FlagField:
-        flags = self.create(forest, block)
-        raw = buf.unpack_array()
-        if raw.shape != flags.field.raw.shape:
-            raise ValidationError(f"serialized flag shape {raw.shape} != expected "
-                                  f"{flags.field.raw.shape}")
-        flags.field.raw[...] = raw
-        return flags
+    def _array(self, flags):
+        return flags.field.raw
 
 
-# ------------------------------------------------------------ ghost exchange
+# ------------------------------------------------------------ ghost rounds
 class GhostPackInfo:
     __slots__ = ("key", "width")
 
@@ -270,134 +303,116 @@ def _field_of(value):
     return getattr(value, "field", value)
 
 
-def _isect(a, b):
-    lo = tuple(max(a[0][i], b[0][i]) for i in range(3))
-    hi = tuple(min(a[1][i], b[1][i]) for i in range(3))
-    if any(lo[i] >= hi[i] for i in range(3)):
-        return None
-    return lo, hi
+class _Box:
+    """Half-open global cell box [lo, hi)."""
+
+    __slots__ = ("lo", "hi")
+
+    def __init__(self, lo, hi):
+        self.lo, self.hi = tuple(lo), tuple(hi)
+
+    def moved(self, delta):
+        return _Box([l + d for l, d in zip(self.lo, delta)], [h + d for h, d in zip(self.hi, delta)])
+
+    def grown(self, w):
+        return _Box([l - w for l in self.lo], [h + w for h in self.hi])
+
+    def clip(self, other):
+        lo = [max(a, b) for a, b in zip(self.lo, other.lo)]
+        hi = [min(a, b) for a, b in zip(self.hi, other.hi)]
+        return _Box(lo, hi) if all(l < h for l, h in zip(lo, hi)) else None
+
+    def window(self, origin, g):
+        """(z, y, x) slices of this box in a field whose interior starts at origin."""
+        return tuple(slice(self.lo[a] - origin[a] + g, self.hi[a] - origin[a] + g)
+                     for a in (2, 1, 0))
 
 
-def _image_box(forest, bid, shift):
-    lo, hi = forest.cell_box(bid)
-    n = forest.global_cells(0)
-    lo = tuple(lo[a] + shift[a] * n[a] for a in range(3))
-    hi = tuple(hi[a] + shift[a] * n[a] for a in range(3))
-    return lo, hi
-
-
-def _slice(view, box, origin, g):
-    lo, hi = box
-    return view[lo[2] - origin[2] + g:hi[2] - origin[2] + g,
-                lo[1] - origin[1] + g:hi[1] - origin[1] + g,
-                lo[0] - origin[0] + g:hi[0] - origin[0] + g]
+def _widths(forest, infos):
+    out = []
+    for info in infos:
+        info = GhostPackInfo(info) if isinstance(info, str) else info
+        w = info.width
+        if w is None:
+            first = next(iter(forest.local_blocks()), None)
+            w = None if first is None else _field_of(first.data[info.key]).g
+        if w is not None and w < 1:
+            raise ValidationError(f"pack width for {info.key!r} must be >= 1")
+        out.append((info.key, w))
+    return sorted(out)
 
 
 def exchange_ghosts(forest, infos, *, tag=110) -> None:
-    """One collective ghost round on host data (ghost.py:202-264): for every
-    unique neighbour image the receiver's box grown by w, intersected with the
-    sender's interior, is copied into the receiver's ghost cells.  Uniform
-    level only.  For a PdfField slot this is the reference meaning (all q
-    components, R-form): the mirror is synced from the device first."""
+    """One collective ghost round on host data (ghost.py:202-264): for each
+    distinct neighbour image (block, periodic shift) of a block, the part of
+    the block's interior that lies in the image's box grown by the pack
+    width lands in the neighbour's ghost cells.  Same-rank images are copied
+    directly, the rest travel in one all-gather.  For a PdfField slot this
+    is the reference meaning (all q components, R-form; the host mirror is
+    synced from the device first)."""
     ctx = forest.ctx
-    if forest.cells_per_block is None:
-        raise ValidationError("forest has no cells_per_block")
-    resolved = []
-    for info in infos:
-        if isinstance(info, str):
-            info = GhostPackInfo(info)
-        width = info.width
-        if width is None:
-            for block in forest.local_blocks():
-                width = _field_of(block.data[info.key]).g
-                break
-        if width is not None and width < 1:
-            raise ValidationError(f"pack width for {info.key!r} must be >= 1")
-        resolved.append((info.key, width))
-    resolved.sort()
-    outgoing = {}
+    period = forest.global_cells(0)
+    packs = _widths(forest, infos)
+    mail = {}
     for block in forest.local_blocks():
-        s_box = forest.cell_box(block.id)
-        seen = {}
-        for rec in block.neighbors:
-            seen[(rec.block_id, rec.shift)] = rec
-        for (nb_id, shift) in sorted(seen):
-            rec = seen[(nb_id, shift)]
-            for key, w in resolved:
-                field = _field_of(block.data[key])
-                r_lo, r_hi = _image_box(forest, nb_id, shift)
-                ghost = (tuple(v - w for v in r_lo), tuple(v + w for v in r_hi))
-                o = _isect(ghost, s_box)
-                if o is None:
+        mine = _Box(*forest.cell_box(block.id))
+        images = sorted({(rec.block_id, rec.shift): rec.rank for rec in block.neighbors}.items())
+        for (nb_id, shift), rank in images:
+            wrap = [s * n for s, n in zip(shift, period)]
+            image = _Box(*forest.cell_box(nb_id)).moved(wrap)
+            for key, w in packs:
+                part = image.grown(w).clip(mine)
+                if part is None:
                     continue
-                data = np.ascontiguousarray(_slice(field.view, o, s_box[0], field.g))
-                back = tuple(-v for v in shift)
-                # receiver-local box: the overlap seen from the receiver's frame
-                n = forest.global_cells(0)
-                r_box = (tuple(o[0][a] - shift[a] * n[a] for a in range(3)),
-                         tuple(o[1][a] - shift[a] * n[a] for a in range(3)))
-                item = (nb_id, key, r_box, data)
-                if rec.rank == ctx.rank:
-                    _unpack(forest, item)
+                field = _field_of(block.data[key])
+                payload = np.ascontiguousarray(field.view[part.window(mine.lo, field.g)])
+                item = (nb_id, key, part.moved([-v for v in wrap]), payload)
+                if rank == ctx.rank:
+                    _deliver(forest, item)
                 else:
-                    outgoing.setdefault(rec.rank, []).append(item)
-                del back
+                    mail.setdefault(rank, []).append(item)
     if ctx.n_ranks > 1:
-        gathered = ctx.all_gather(outgoing)
-        for src in sorted(gathered):
-            for item in gathered[src].get(ctx.rank, []):
-                _unpack(forest, item)
+        posted = ctx.all_gather(mail)
+        for sender in sorted(posted):
+            for item in posted[sender].get(ctx.rank, ()):
+                _deliver(forest, item)
 
 
-def _unpack(forest, item):
-    nb_id, key, r_box, data = item
-    block = forest.blocks.get(nb_id)
-    if block is None:
+def _deliver(forest, item):
+    nb_id, key, box, payload = item
+    if nb_id not in forest.blocks:
         raise ValidationError(f"ghost data for non-local block {nb_id}")
-    field = _field_of(block.data[key])
-    lo, _ = forest.cell_box(nb_id)
-    _slice(field.view, r_box, lo, field.g)[...] = data
+    field = _field_of(forest.blocks[nb_id].data[key])
+    origin = forest.cell_box(nb_id)[0]
+    field.view[box.window(origin, field.g)] = payload
 
 
 def gather_slice(forest, key, lo, hi, level=0):
-    """Dense (z, y, x, f) array of the global cell box [lo, hi) on rank 0
-    (gather.py:10-79); None on other ranks."""
-    ctx = forest.ctx
-    lo = tuple(int(v) for v in lo)
-    hi = tuple(int(v) for v in hi)
+    """Dense (z, y, x, f) array of the global cell box [lo, hi) on rank 0,
+    None elsewhere (gather.py:10-79)."""
     if level != 0:
         raise ValidationError("only level 0 exists on the B200 path")
+    want = _Box([int(v) for v in lo], [int(v) for v in hi])
     ext = forest.global_cells(level)
-    for a in range(3):
-        if not (0 <= lo[a] < hi[a] <= ext[a]):
-            raise ValidationError(f"slice box {lo}..{hi} outside the level-{level} grid {ext}")
-    contributions = []
+    if not all(0 <= want.lo[a] < want.hi[a] <= ext[a] for a in range(3)):
+        raise ValidationError(f"slice box {want.lo}..{want.hi} outside the level-{level} grid {ext}")
+    pieces = []
     for block in forest.local_blocks():
-        blo, bhi = forest.cell_box(block.id)
-        olo = tuple(max(blo[a], lo[a]) for a in range(3))
-        ohi = tuple(min(bhi[a], hi[a]) for a in range(3))
-        if any(olo[a] >= ohi[a] for a in range(3)):
-            continue
-        view = _field_of(block.data[key]).interior
-        sub = view[olo[2] - blo[2]:ohi[2] - blo[2], olo[1] - blo[1]:ohi[1] - blo[1],
-                   olo[0] - blo[0]:ohi[0] - blo[0]]
-        contributions.append((olo, np.ascontiguousarray(sub)))
-    gathered = ctx.all_gather(contributions)
-    nf = dtype = None
-    for rank in sorted(gathered):
-        for _, arr in gathered[rank]:
-            nf, dtype = arr.shape[3], arr.dtype
-            break
-        if nf is not None:
-            break
-    if nf is None:
+        own = _Box(*forest.cell_box(block.id))
+        part = own.clip(want)
+        if part is not None:
+            inner = _field_of(block.data[key]).interior
+            pieces.append((part.lo, np.ascontiguousarray(inner[part.window(own.lo, 0)])))
+    everyone = forest.ctx.all_gather(pieces)
+    arrays = [arr for r in sorted(everyone) for _, arr in everyone[r]]
+    if not arrays:
         raise ValidationError("slice box covers no stored blocks")
-    if ctx.rank != 0:
+    if forest.ctx.rank != 0:
         return None
-    out = np.zeros((hi[2] - lo[2], hi[1] - lo[1], hi[0] - lo[0], nf), dtype=dtype)
-    for rank in sorted(gathered):
-        for olo, arr in gathered[rank]:
-            out[olo[2] - lo[2]:olo[2] - lo[2] + arr.shape[0],
-                olo[1] - lo[1]:olo[1] - lo[1] + arr.shape[1],
-                olo[0] - lo[0]:olo[0] - lo[0] + arr.shape[2]] = arr
+    shape = tuple(want.hi[a] - want.lo[a] for a in (2, 1, 0)) + (arrays[0].shape[3],)
+    out = np.zeros(shape, dtype=arrays[0].dtype)
+    for r in sorted(everyone):
+        for plo, arr in everyone[r]:
+            at = _Box(plo, [plo[a] + arr.shape[2 - a] for a in range(3)])
+            out[at.window(want.lo, 0)] = arr
     return out

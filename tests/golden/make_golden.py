@@ -227,6 +227,38 @@ def make_slot():
     print("slot:", len(slot_cases()), "collide cases")
 
 
+OWNERSHIP_FORESTS = [  # (root_dims, d, periodic, n_ranks)
+    ((1, 1, 8), 3, (True, True, False), 8), ((1, 1, 8), 3, (True, True, True), 3),
+    ((2, 2, 2), 3, (True, False, True), 3), ((3, 2, 5), 3, (False, True, False), 7),
+    ((4, 3, 1), 2, (True, False, False), 5), ((5, 1, 1), 2, (True, True, False), 2),
+    ((1, 1, 1), 3, (True, True, True), 1), ((2, 3, 4), 3, (True, True, True), 24),
+]
+
+
+def make_ownership():
+    """Rank ownership + neighbour records: the reference's own balance.py
+    routines and create_forest on a set of root grids and rank counts."""
+    from blocksim import balance as B
+    from blocksim.blockforest import create_forest
+    from blocksim.runtime import SimRuntime
+    parts = {}
+    for n in range(0, 41):
+        for p in range(1, 13):
+            parts[f"{n},{p}"] = B.partition_curve([1.0] * n, p)
+    forests = []
+    for dims, d, per, ranks in OWNERSHIP_FORESTS:
+        def prog(ctx):
+            f = create_forest(ctx, (0, 0, 0) + tuple(float(v) for v in dims), dims, d=d,
+                              periodic=per, cells_per_block=(2, 2, 2 if d == 3 else 1))
+            return [[b.id.root, [[list(r.direction), r.block_id.root, r.rank, list(r.shift)]
+                                 for r in b.neighbors]] for b in f.local_blocks()]
+        res = SimRuntime(ranks, seed=0).run(prog)
+        forests.append({"dims": dims, "d": d, "periodic": per, "ranks": ranks,
+                        "blocks": {str(r): res[r] for r in range(ranks)}})
+    (HERE / "ownership.json").write_text(json.dumps({"partition": parts, "forests": forests}))
+    print("ownership:", len(parts), "partitions,", len(forests), "forests")
+
+
 def make_units():
     """Reference unit functions on seeded random cells."""
     import blocksim.lbm as L
@@ -280,6 +312,8 @@ if __name__ == "__main__":
         make_snapshot()
     elif args == ["slot"]:
         make_slot()
+    elif args == ["ownership"]:
+        make_ownership()
     elif args == ["coupling"]:
         make_coupling()
     else:
@@ -288,3 +322,4 @@ if __name__ == "__main__":
             make_snapshot()
             make_coupling()
             make_slot()
+            make_ownership()

@@ -147,9 +147,9 @@ def test_rankbox_rejects_non_slab_partitions():
 
 
 def test_balance_matches_reference_rule():
-    assert balance.partition_curve([1.0] * 8, 3) == [0, 0, 0, 1, 1, 2, 2, 2]
-    assert balance.partition_curve([1.0] * 4, 4) == [0, 1, 2, 3]
-    keys = [balance.morton_key((x, y, 0), 0, 2, 2) for y in range(2) for x in range(2)]
+    assert balance.owners_along_curve(8, 3) == [0, 0, 0, 1, 1, 2, 2, 2]
+    assert balance.owners_along_curve(4, 4) == [0, 1, 2, 3]
+    keys = [balance.morton_position((x, y, 0), 2) for y in range(2) for x in range(2)]
     assert keys == [0, 1, 2, 3]
 
 
