@@ -28,6 +28,7 @@
  *                       (field/core.py:34-70; "fzyx" raw shape (q,Z,Y,X)).
  *   lbm_build_cellmask  build_index_lists + sweep-time flag validation
  *                       (lbm/boundary.py:48-97, lbm/sweep.py:124-136).
+ *   lbm_map_spheres     map_bodies' voxeliser (coupling/mapping.py:100-140).
  *   lbm_refresh_fluid_mask  the per-sweep fluid mask of flags edited after
  *                       freeze() (lbm/sweep.py:124-136; links stay frozen).
  *   lbm_collide_cells / lbm_equilibrium_cells / lbm_macroscopic_cells
@@ -302,6 +303,22 @@ int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags,
 int lbm_refresh_fluid_mask(const lbm_grid_t* g, const uint32_t* flags,
                            const uint32_t bits[5], const uint32_t* cellmask_in,
                            uint32_t* cellmask_out, int* err, void* stream);
+
+/* Body coverage (ABI 5): the device voxeliser of map_bodies
+ * (coupling/mapping.py:100-140) for n_blocks ghost-inclusive blocks of
+ * cells[0] x cells[1] x cells[2] interior cells.  frame (n_blocks, 6): centre
+ * of each block's cell (0, 0, 0) and its spacings; the block's spheres are
+ * spheres[first[b] .. first[b+1]) as (x, y, z, r) rows with uids[] in
+ * ascending order (Local bodies and pre-shifted Ghost copies).  owner
+ * (n_blocks, nz+2, ny+2, nx+2) receives the uid of the first sphere whose
+ * interior strictly holds the cell centre (reference arithmetic and bounding
+ * window), or -1; with flags (same shape, may be NULL) only cells with
+ * flags & fluid_bits can be claimed.  All arrays are DEVICE pointers except
+ * `cells`. */
+int lbm_map_spheres(int n_blocks, const int32_t cells[3], const double* frame,
+                    const int32_t* first, const double* spheres, const int64_t* uids,
+                    const uint32_t* flags, uint32_t fluid_bits, int64_t* owner,
+                    void* stream);
 
 /* Combined masks of a moving-body sweep: cellmask_out = cellmask_in with
  * LBM_MASK_FLUID cleared on covered cells (owner >= 0; they skip the

@@ -1,20 +1,20 @@
-"""Rigid bodies on the block forest: the data model the moving-boundary sweep
-reads (host side; bodies are a few hundred bytes each).
+"""Rigid spheres on the block forest: the body data the moving-boundary
+sweep reads (host side; a body is a few hundred bytes).
 
-Same names, semantics and snapshot byte format as the reference's body
-storage (pkg/src/blocksim/rpd/body.py:63-202, storage.py:24-313,
-step.py:123-243): spheres with kinematic state, one BodyStorage per block
-holding Local bodies (centre inside the block) and Ghost copies (pre-shifted
-periodic images of bodies reaching into the block), collective
-`add_sphere`, and `sync_bodies` (ownership migration, then a full ghost
-rebuild).  Cross-rank traffic goes through the rank context's all_gather;
-every rank applies the same deterministic order, so ghosts are bitwise
-copies of their masters as in the reference.
+Names and semantics follow the reference's rigid-body storage
+(pkg/src/blocksim/rpd/body.py:63-202, storage.py:24-313, step.py:123-243):
+each block keeps a BodyStorage with its Local bodies (centre inside the
+block) and Ghost copies of bodies whose bounding sphere (+ contact
+threshold) reaches into it, stored at the position of the periodic image
+that block sees.  `add_sphere` is collective; `sync_bodies` migrates bodies
+whose centre left their block, then rebuilds every ghost copy.  Cross-rank
+traffic is one all_gather per phase, unpacked in rank order, so ghosts are
+bitwise copies of their masters.
 
-Not here: the DEM contact pipeline (rpd/contact.py, step.time_step) and
-half spaces - the B200 path couples the fluid to bodies moved by the caller.
+Not here: the DEM contact pipeline and integrators (rpd/contact.py,
+step.time_step) and half spaces: on the B200 path bodies are moved by the
+caller between coupled steps.
 """
-from __future__ import annotations
 
 import math
 
@@ -26,393 +26,364 @@ LOCAL = "Local"
 GHOST = "Ghost"
 
 
-def _vec3(value, name):
+def _vector(value, n, what):
     v = np.array(value, dtype=np.float64).reshape(-1)
-    if v.shape != (3,):
-        raise ValidationError(f"{name} must have 3 components, got {value!r}")
+    if v.size != n:
+        raise ValidationError(f"{what} needs {n} components, got {value!r}")
     return v
 
 
-def _unit_quat(q):
-    q = np.asarray(q, dtype=np.float64).reshape(-1)
-    if q.shape != (4,):
-        raise ValidationError(f"quaternion must have 4 components, got {q.shape}")
-    n = math.sqrt(float(np.dot(q, q)))
-    if not (n > 1e-8 and math.isfinite(n)):
-        raise ValidationError("quaternion norm too small to normalize")
+def _positive(value, what):
+    v = float(value)
+    if not (v > 0.0 and math.isfinite(v)):
+        raise ValidationError(f"{what} must be positive and finite, got {value!r}")
+    return v
+
+
+def _normalised(quat):
+    q = _vector(quat, 4, "orientation")
+    n = math.sqrt(float(q @ q))
+    if not (math.isfinite(n) and n > 1e-8):
+        raise ValidationError("orientation quaternion has (near) zero norm")
     return q / n
 
 
 class Sphere:
+    """Sphere shape: radius, bounding radius, body-frame inertia."""
+
     __slots__ = ("radius",)
     kind = "sphere"
 
     def __init__(self, radius):
-        radius = float(radius)
-        if not (radius > 0 and math.isfinite(radius)):
-            raise ValidationError(f"sphere radius must be positive, got {radius}")
-        self.radius = radius
+        self.radius = _positive(radius, "sphere radius")
 
-    @property
-    def bounding_radius(self):
-        return self.radius
+    bounding_radius = property(lambda self: self.radius)
 
     def inertia(self, mass):
-        i = 0.4 * mass * self.radius * self.radius
-        return np.diag([i, i, i]), np.diag([1.0 / i] * 3)
+        """(I, I^-1) of a solid sphere: 2/5 m r^2 on the diagonal."""
+        moment = 0.4 * mass * self.radius * self.radius
+        return np.eye(3) * moment, np.eye(3) * (1.0 / moment)
 
     def __repr__(self):
-        return f"Sphere({self.radius})"
+        return "Sphere(%r)" % (self.radius,)
+
+
+# per-body vectors that start at zero, and the kinematic ones given at creation
+_ZEROED = ("force", "torque", "hydrodynamic_force", "hydrodynamic_torque", "_accel", "_ang_accel")
 
 
 class RigidBody:
-    """Sphere + kinematic state + accumulators (body.py:145-202)."""
+    """A sphere with kinematic state, accumulators and its storage label
+    (Local master or Ghost copy, and the owning rank)."""
 
-    __slots__ = ("uid", "shape", "position", "orientation", "linear_velocity",
-                 "angular_velocity", "force", "torque", "mass", "inv_mass", "inertia_body",
-                 "inv_inertia_body", "classification", "owner_rank", "hydrodynamic_force",
-                 "hydrodynamic_torque", "_accel", "_ang_accel", "_kicked", "_image")
+    __slots__ = ("uid", "shape", "mass", "inv_mass", "inertia_body", "inv_inertia_body",
+                 "classification", "owner_rank", "position", "orientation", "linear_velocity",
+                 "angular_velocity", "_kicked", "_image") + _ZEROED
 
     def __init__(self, uid, shape, position, *, orientation=(1.0, 0.0, 0.0, 0.0),
                  linear_velocity=(0.0, 0.0, 0.0), angular_velocity=(0.0, 0.0, 0.0), mass=None,
                  classification=LOCAL, owner_rank=0):
         if classification not in (LOCAL, GHOST):
-            raise ValidationError(f"unknown classification {classification!r}")
-        if mass is None or not (float(mass) > 0 and math.isfinite(float(mass))):
-            raise ValidationError(f"finite body needs a positive mass, got {mass}")
-        self.uid = int(uid)
-        self.shape = shape
-        self.position = _vec3(position, "position")
-        self.orientation = _unit_quat(orientation)
-        self.linear_velocity = _vec3(linear_velocity, "linear_velocity")
-        self.angular_velocity = _vec3(angular_velocity, "angular_velocity")
-        self.force = np.zeros(3)
-        self.torque = np.zeros(3)
-        self.mass = float(mass)
+            raise ValidationError(f"classification must be {LOCAL!r} or {GHOST!r}, "
+                                  f"got {classification!r}")
+        if mass is None:
+            raise ValidationError("a body needs a mass")
+        self.uid, self.shape = int(uid), shape
+        self.mass = _positive(mass, "body mass")
         self.inv_mass = 1.0 / self.mass
         self.inertia_body, self.inv_inertia_body = shape.inertia(self.mass)
-        self.classification = classification
-        self.owner_rank = int(owner_rank)
-        self.hydrodynamic_force = np.zeros(3)
-        self.hydrodynamic_torque = np.zeros(3)
-        self._accel = np.zeros(3)
-        self._ang_accel = np.zeros(3)
+        self.classification, self.owner_rank = classification, int(owner_rank)
+        self.position = _vector(position, 3, "position")
+        self.orientation = _normalised(orientation)
+        self.linear_velocity = _vector(linear_velocity, 3, "linear_velocity")
+        self.angular_velocity = _vector(angular_velocity, 3, "angular_velocity")
+        for name in _ZEROED:
+            setattr(self, name, np.zeros(3))
         self._kicked = False
         self._image = (0, 0, 0)
 
-    @property
-    def is_finite(self):
-        return True
-
-    @property
-    def bounding_radius(self):
-        return self.shape.bounding_radius
+    is_finite = property(lambda self: True)
+    bounding_radius = property(lambda self: self.shape.bounding_radius)
 
     def velocity_at(self, point):
+        """Rigid-body velocity v + w x (p - x) at a point."""
         return self.linear_velocity + np.cross(self.angular_velocity, point - self.position)
+
+    def replica(self, classification, owner_rank, offset=None):
+        """A copy of the kinematic state (a ghost or a migrated master),
+        optionally moved by `offset`."""
+        out = RigidBody(self.uid, self.shape, self.position if offset is None
+                        else self.position - offset, orientation=self.orientation,
+                        linear_velocity=self.linear_velocity,
+                        angular_velocity=self.angular_velocity, mass=self.mass,
+                        classification=classification, owner_rank=owner_rank)
+        return out
 
     def __repr__(self):
         return f"RigidBody(uid={self.uid}, {self.shape!r}, {self.classification}@{self.owner_rank})"
 
 
-class BodyStorage:
-    __slots__ = ("bodies",)
+class BodyStorage(dict):
+    """The bodies one block stores: a uid -> body dict (`bodies` is the
+    reference's name for the same mapping)."""
 
-    def __init__(self):
-        self.bodies = {}
+    bodies = property(lambda self: self)
 
     def add(self, body):
-        if body.uid in self.bodies:
-            raise ValidationError(f"uid {body.uid} already stored on this block")
-        self.bodies[body.uid] = body
+        if body.uid in self:
+            raise ValidationError(f"body {body.uid} is already stored on this block")
+        self[body.uid] = body
 
-    def remove(self, uid):
-        return self.bodies.pop(uid)
+    remove = dict.pop
 
-    def get(self, uid):
-        return self.bodies.get(uid)
+    def _labelled(self, label):
+        return [b for _, b in sorted(self.items()) if b.classification == label]
 
-    def local(self):
-        return [self.bodies[u] for u in sorted(self.bodies)
-                if self.bodies[u].classification == LOCAL]
-
-    def ghosts(self):
-        return [self.bodies[u] for u in sorted(self.bodies)
-                if self.bodies[u].classification == GHOST]
+    local = lambda self: self._labelled(LOCAL)      # noqa: E731
+    ghosts = lambda self: self._labelled(GHOST)     # noqa: E731
 
     def clear_ghosts(self):
-        for uid in [u for u, b in self.bodies.items() if b.classification == GHOST]:
-            del self.bodies[uid]
+        for uid in [u for u, b in self.items() if b.classification == GHOST]:
+            del self[uid]
 
-    def __contains__(self, uid):
-        return uid in self.bodies
 
-    def __len__(self):
-        return len(self.bodies)
+# ----------------------------------------------------- body records
+# A body's record in snapshots and messages (storage.py:60-76 layout): uid,
+# shape kind (0 = sphere), radius, mass, eight 3/4-vectors, the kick flag.
+_VECTORS = ("position", "orientation", "linear_velocity", "angular_velocity",
+            "hydrodynamic_force", "hydrodynamic_torque", "_accel", "_ang_accel")
 
 
 def pack_body(buf, body):
-    """Snapshot / message record of one body (storage.py:60-76)."""
-    buf.pack_int(body.uid)
-    buf.pack_int(0)                       # shape kind: sphere
-    buf.pack_float(body.shape.radius)
-    buf.pack_float(body.mass)
-    for v in (body.position, body.orientation, body.linear_velocity, body.angular_velocity,
-              body.hydrodynamic_force, body.hydrodynamic_torque, body._accel, body._ang_accel):
-        buf.pack_floats(v)
-    buf.pack_bool(body._kicked)
+    for v in (body.uid, 0):
+        buf.pack_int(v)
+    for v in (body.shape.radius, body.mass):
+        buf.pack_float(v)
+    for name in _VECTORS:
+        buf.pack_floats(getattr(body, name))
+    buf.pack_bool(bool(body._kicked))
 
 
 def unpack_body(buf, *, classification=LOCAL, owner_rank=0):
-    uid = buf.unpack_int()
-    if buf.unpack_int() != 0:
+    uid, kind = buf.unpack_int(), buf.unpack_int()
+    if kind != 0:
         raise ValidationError("only sphere bodies exist on the B200 path")
-    shape = Sphere(buf.unpack_float())
-    mass = buf.unpack_float()
-    body = RigidBody(uid, shape, buf.unpack_floats(), orientation=buf.unpack_floats(),
-                     linear_velocity=buf.unpack_floats(), angular_velocity=buf.unpack_floats(),
-                     mass=mass, classification=classification, owner_rank=owner_rank)
-    body.hydrodynamic_force = np.array(buf.unpack_floats())
-    body.hydrodynamic_torque = np.array(buf.unpack_floats())
-    body._accel = np.array(buf.unpack_floats())
-    body._ang_accel = np.array(buf.unpack_floats())
+    radius, mass = buf.unpack_float(), buf.unpack_float()
+    vec = {name: np.array(buf.unpack_floats()) for name in _VECTORS}
+    body = RigidBody(uid, Sphere(radius), vec["position"], orientation=vec["orientation"],
+                     linear_velocity=vec["linear_velocity"],
+                     angular_velocity=vec["angular_velocity"], mass=mass,
+                     classification=classification, owner_rank=owner_rank)
+    for name in _VECTORS[4:]:
+        setattr(body, name, vec[name])
     body._kicked = buf.unpack_bool()
     return body
 
 
-def _contains(aabb, p):
-    """Half-open block box (lower faces inclusive)."""
-    return (aabb[0] <= p[0] < aabb[3] and aabb[1] <= p[1] < aabb[4]
-            and aabb[2] <= p[2] < aabb[5])
-
-
 class BodyStorageHandler:
-    """Forest data handler of the body slot (storage.py:94-152); snapshots
-    carry Local bodies only (ghosts are rebuilt by sync_bodies)."""
+    """Forest slot handler: one BodyStorage per block; images carry the
+    Local bodies only (sync_bodies rebuilds ghosts)."""
 
     def __init__(self, contact_threshold=None):
-        if contact_threshold is not None and not contact_threshold >= 0:
+        if not (contact_threshold is None or contact_threshold >= 0):
             raise ValidationError(f"contact threshold must be >= 0, got {contact_threshold}")
-        self.fixed_threshold = contact_threshold
-        self.auto_threshold = 0.0
+        self.fixed_threshold, self.auto_threshold = contact_threshold, 0.0
 
     @property
     def contact_threshold(self):
-        return self.fixed_threshold if self.fixed_threshold is not None else self.auto_threshold
+        return self.auto_threshold if self.fixed_threshold is None else self.fixed_threshold
 
-    def create(self, forest, block):
+    @staticmethod
+    def create(forest, block):
         return BodyStorage()
 
-    def serialize(self, forest, block, storage, buf):
-        bodies = storage.local()
-        buf.pack_int(len(bodies))
-        for body in bodies:
+    @staticmethod
+    def serialize(forest, block, storage, buf):
+        masters = storage.local()
+        buf.pack_int(len(masters))
+        for body in masters:
             pack_body(buf, body)
 
-    def deserialize(self, forest, block, buf):
-        storage = BodyStorage()
-        for _ in range(buf.unpack_int()):
-            storage.add(unpack_body(buf, owner_rank=forest.ctx.rank))
-        return storage
+    @staticmethod
+    def deserialize(forest, block, buf):
+        count = buf.unpack_int()
+        bodies = [unpack_body(buf, owner_rank=forest.ctx.rank) for _ in range(count)]
+        out = BodyStorage()
+        for body in bodies:
+            out.add(body)
+        return out
 
 
 def register_bodies(forest, key="bodies", *, contact_threshold=None):
-    """Collective: attach a body storage slot to every block."""
+    """Collective: a body storage slot on every block."""
     forest.register_data(key, BodyStorageHandler(contact_threshold))
     return key
 
 
 def handler_of(forest, key):
-    h = forest.handlers.get(key)
-    if not isinstance(h, BodyStorageHandler):
-        raise ValidationError(f"slot {key!r} is not a body storage")
-    return h
+    handler = forest.handlers.get(key)
+    if isinstance(handler, BodyStorageHandler):
+        return handler
+    raise ValidationError(f"slot {key!r} is not a body storage")
 
 
-def _next_uid(forest, key):
-    top = -1
+def _stored(forest, key, label=None):
     for block in forest.local_blocks():
-        for uid in block.data[key].bodies:
-            top = max(top, uid)
-    return int(forest.ctx.all_reduce((top,), "max")[0]) + 1
+        for _, body in sorted(block.data[key].bodies.items()):
+            if label is None or body.classification == label:
+                yield block, body
 
 
-def _refresh_threshold(forest, key):
-    smallest = math.inf
-    for block in forest.local_blocks():
-        for body in block.data[key].local():
-            smallest = min(smallest, body.bounding_radius)
-    smallest = forest.ctx.all_reduce((smallest,), "min")[0]
-    handler_of(forest, key).auto_threshold = 0.1 * smallest if math.isfinite(smallest) else 0.0
+def _inside(box, p):
+    """Half-open AABB membership (lower faces belong to the box)."""
+    return all(box[a] <= p[a] < box[a + 3] for a in range(3))
 
 
 def add_sphere(forest, position, radius, *, key="bodies", mass=None, density=None,
                velocity=(0.0, 0.0, 0.0), angular_velocity=(0.0, 0.0, 0.0),
                orientation=(1.0, 0.0, 0.0, 0.0)):
-    """Collective: store a sphere on the block containing its centre; returns
-    its uid (the same on every rank)."""
+    """Collective: a new sphere, stored on the block whose box holds its
+    centre; the uid (one past the largest in use) is returned on every rank."""
     if (mass is None) == (density is None):
         raise ValidationError("give exactly one of mass or density")
     shape = Sphere(radius)
     if density is not None:
-        if not float(density) > 0:
-            raise ValidationError(f"density must be positive, got {density}")
-        mass = float(density) * 4.0 / 3.0 * math.pi * shape.radius ** 3
-    uid = _next_uid(forest, key)
-    mine = 0
-    for block in forest.local_blocks():
-        if _contains(forest.block_aabb(block.id), position):
-            block.data[key].add(RigidBody(uid, shape, position, orientation=orientation,
-                                          linear_velocity=velocity,
-                                          angular_velocity=angular_velocity, mass=mass,
-                                          owner_rank=forest.ctx.rank))
-            mine = 1
-            break
-    if int(forest.ctx.all_reduce((mine,), "sum")[0]) != 1:
+        mass = _positive(density, "density") * 4.0 / 3.0 * math.pi * shape.radius ** 3
+    top = max((uid for block in forest.local_blocks() for uid in block.data[key].bodies),
+              default=-1)
+    uid = int(forest.ctx.all_reduce((top,), "max")[0]) + 1
+    home = next((b for b in forest.local_blocks() if _inside(forest.block_aabb(b.id), position)),
+                None)
+    if home is not None:
+        home.data[key].add(RigidBody(uid, shape, position, orientation=orientation,
+                                     linear_velocity=velocity, angular_velocity=angular_velocity,
+                                     mass=mass, owner_rank=forest.ctx.rank))
+    if int(forest.ctx.all_reduce((int(home is not None),), "sum")[0]) != 1:
         raise ValidationError(f"sphere center {tuple(position)} is outside the domain")
-    _refresh_threshold(forest, key)
+    smallest = min((b.bounding_radius for _, b in _stored(forest, key, LOCAL)), default=math.inf)
+    smallest = forest.ctx.all_reduce((smallest,), "min")[0]
+    handler_of(forest, key).auto_threshold = 0.1 * smallest if math.isfinite(smallest) else 0.0
     return uid
 
 
 def local_bodies(forest, key="bodies"):
-    out = []
-    for block in forest.local_blocks():
-        out.extend(block.data[key].local())
-    out.sort(key=lambda b: b.uid)
-    return out
+    return sorted((b for _, b in _stored(forest, key, LOCAL)), key=lambda b: b.uid)
 
 
 def ghost_bodies(forest, key="bodies"):
-    out = []
-    for block in forest.local_blocks():
-        out.extend(block.data[key].ghosts())
-    return out
+    return [b for _, b in _stored(forest, key, GHOST)]
 
 
 def find_body(forest, uid, key="bodies"):
-    for block in forest.local_blocks():
-        body = block.data[key].get(uid)
-        if body is not None and body.classification == LOCAL:
-            return body
-    return None
+    return next((b for _, b in _stored(forest, key, LOCAL) if b.uid == uid), None)
 
 
 # ---------------------------------------------------------------- sync
-def _extents(forest):
-    x0, y0, z0, x1, y1, z1 = forest.domain
-    return np.array([x1 - x0, y1 - y0, z1 - z0])
+class _Mailbox:
+    """Items for blocks of this rank are applied at once, the rest travel
+    in one all_gather and are applied in sender-rank order."""
+
+    def __init__(self, ctx, apply):
+        self.ctx, self.apply, self.out = ctx, apply, {}
+
+    def post(self, rank, item):
+        if rank == self.ctx.rank:
+            self.apply(item)
+        else:
+            self.out.setdefault(rank, []).append(item)
+
+    def flush(self):
+        if self.ctx.n_ranks > 1:
+            everyone = self.ctx.all_gather(self.out)
+            for sender in sorted(everyone):
+                for item in everyone[sender].get(self.ctx.rank, ()):
+                    self.apply(item)
+        self.out = {}
 
 
-def _images(block):
-    """Unique (neighbour block id, shift, rank), deterministic order."""
-    seen = {}
-    for rec in block.neighbors:
-        seen[(rec.block_id, rec.shift)] = rec.rank
-    return [(bid, shift, seen[(bid, shift)]) for bid, shift in sorted(seen)]
-
-
-def _shifted_aabb(forest, bid, shift, ext):
-    b = forest.block_aabb(bid)
-    return (b[0] + shift[0] * ext[0], b[1] + shift[1] * ext[1], b[2] + shift[2] * ext[2],
-            b[3] + shift[0] * ext[0], b[4] + shift[1] * ext[1], b[5] + shift[2] * ext[2])
-
-
-def _sphere_overlaps(aabb, c, r):
-    d2 = 0.0
-    for a in range(3):
-        if c[a] < aabb[a]:
-            d2 += (aabb[a] - c[a]) ** 2
-        elif c[a] > aabb[a + 3]:
-            d2 += (c[a] - aabb[a + 3]) ** 2
-    return d2 <= r * r
-
-
-def _copy(body, classification, owner):
-    out = RigidBody(body.uid, body.shape, body.position.copy(),
-                    orientation=body.orientation.copy(),
-                    linear_velocity=body.linear_velocity.copy(),
-                    angular_velocity=body.angular_velocity.copy(), mass=body.mass,
-                    classification=classification, owner_rank=owner)
+def _neighbour_images(forest, block, extent):
+    """(block id, shift, rank, shifted AABB) of each distinct neighbour
+    image, in (id, shift) order."""
+    seen = {(r.block_id, r.shift): r.rank for r in block.neighbors}
+    out = []
+    for (bid, shift), rank in sorted(seen.items()):
+        move = np.asarray(shift, dtype=np.float64) * extent
+        box = np.asarray(forest.block_aabb(bid), dtype=np.float64) + np.concatenate([move, move])
+        out.append((bid, shift, rank, box))
     return out
 
 
-def _add_ghost(forest, key, bid, ghost):
-    block = forest.blocks.get(bid)
-    if block is None:
-        raise SyncError(f"ghost of body {ghost.uid} targets non-local block {bid}")
-    storage = block.data[key]
-    if ghost.uid in storage:
-        raise SyncError(f"two images of body {ghost.uid} meet in one block; the domain is too "
-                        "small for its size")
-    storage.add(ghost)
+def _gap2(box, c):
+    """Squared distance from point c to an AABB (0 inside)."""
+    d2 = 0.0
+    for a in range(3):
+        gap = max(box[a] - c[a], 0.0, c[a] - box[a + 3])
+        if gap > 0.0:
+            d2 += gap * gap
+    return d2
 
 
 def sync_bodies(forest, *, key="bodies"):
-    """Collective (step.py:136-232): migrate ownership of bodies whose centre
-    left their block (periodic wrap by whole domain extents), then rebuild
-    every ghost copy (each Local body on every neighbour image its bounding
-    sphere + contact threshold touches)."""
+    """Collective: (1) a body whose centre left its block moves to the
+    neighbour image that now holds it (position wrapped by whole domain
+    extents); (2) every ghost is dropped and rebuilt from the Local bodies
+    whose bounding sphere + contact threshold reaches a neighbour image."""
     ctx = forest.ctx
-    me = ctx.rank
-    threshold = handler_of(forest, key).contact_threshold
-    ext = _extents(forest)
+    lo, hi = np.asarray(forest.domain[:3]), np.asarray(forest.domain[3:])
+    extent = hi - lo
+    reach_extra = handler_of(forest, key).contact_threshold
     for block in forest.local_blocks():
         block.data[key].clear_ghosts()
 
-    outgoing = {}
+    def adopt(item):
+        bid, body = item
+        if bid not in forest.blocks:
+            raise SyncError(f"body {body.uid} migrated to non-local block {bid}")
+        body.owner_rank = ctx.rank
+        forest.blocks[bid].data[key].add(body)
+
+    movers = _Mailbox(ctx, adopt)
     for block in forest.local_blocks():
-        box = forest.block_aabb(block.id)
+        own_box = forest.block_aabb(block.id)
         for body in block.data[key].local():
-            if _contains(box, body.position):
+            if _inside(own_box, body.position):
                 continue
-            target = None
-            for bid, shift, rank in _images(block):
-                if _contains(_shifted_aabb(forest, bid, shift, ext), body.position):
-                    target = (bid, shift, rank)
-                    break
-            if target is None:
+            dest = next(((bid, shift, rank) for bid, shift, rank, box in
+                         _neighbour_images(forest, block, extent)
+                         if _inside(box, body.position)), None)
+            if dest is None:
                 raise SyncError(f"body {body.uid} moved farther than one block in one step "
                                 "(or left the domain)")
-            bid, shift, rank = target
+            bid, shift, rank = dest
             block.data[key].remove(body.uid)
             if any(shift):
-                body.position = body.position - np.array(shift, dtype=np.float64) * ext
-            if rank == me:
-                body.owner_rank = me
-                forest.blocks[bid].data[key].add(body)
-            else:
-                outgoing.setdefault(rank, []).append((bid, body))
-    if ctx.n_ranks > 1:
-        got = ctx.all_gather(outgoing)
-        for src in sorted(got):
-            for bid, body in got[src].get(me, []):
-                body.owner_rank = me
-                block = forest.blocks.get(bid)
-                if block is None:
-                    raise SyncError(f"body {body.uid} migrated to non-local block {bid}")
-                block.data[key].add(body)
+                body.position = body.position - np.asarray(shift, dtype=np.float64) * extent
+            movers.post(rank, (bid, body))
+    movers.flush()
 
-    outgoing = {}
+    def place(item):
+        bid, ghost = item
+        if bid not in forest.blocks:
+            raise SyncError(f"ghost of body {ghost.uid} targets non-local block {bid}")
+        storage = forest.blocks[bid].data[key]
+        if ghost.uid in storage:
+            raise SyncError(f"two images of body {ghost.uid} meet in one block; the domain is "
+                            "too small for its size")
+        storage.add(ghost)
+
+    ghosts = _Mailbox(ctx, place)
     for block in forest.local_blocks():
+        images = _neighbour_images(forest, block, extent)
         for body in block.data[key].local():
-            reach = body.bounding_radius + threshold
-            for bid, shift, rank in _images(block):
-                if not _sphere_overlaps(_shifted_aabb(forest, bid, shift, ext), body.position,
-                                        reach):
+            reach = body.bounding_radius + reach_extra
+            for bid, shift, rank, box in images:
+                if _gap2(box, body.position) > reach * reach:
                     continue
                 if bid == block.id:
                     raise SyncError(f"body {body.uid} overlaps its own periodic image; the "
                                     "domain is too small for its size")
-                ghost = _copy(body, GHOST, me)
-                if any(shift):
-                    ghost.position = ghost.position - np.array(shift, dtype=np.float64) * ext
+                offset = np.asarray(shift, dtype=np.float64) * extent if any(shift) else None
+                ghost = body.replica(GHOST, ctx.rank, offset)
                 ghost._image = tuple(shift)
-                if rank == me:
-                    _add_ghost(forest, key, bid, ghost)
-                else:
-                    outgoing.setdefault(rank, []).append((bid, ghost))
-    if ctx.n_ranks > 1:
-        got = ctx.all_gather(outgoing)
-        for src in sorted(got):
-            for bid, ghost in got[src].get(me, []):
-                _add_ghost(forest, key, bid, ghost)
+                ghosts.post(rank, (bid, ghost))
+    ghosts.flush()

@@ -320,6 +320,44 @@ __global__ void k_moving_masks(KGrid g, const uint32_t* __restrict__ cm_in,
     if (n) atomicAdd(n_links, n);
 }
 
+// Body coverage of ghost-inclusive blocks (coupling/mapping.py:100-140): the
+// cell centre c = c0 + h (i - 1) (per axis, the reference's numpy
+// expression, every op rounded) is covered by the first sphere in uid order
+// with p - r <= c < p + r on every axis (the reference's searchsorted
+// window) and ((cx-px)^2 + (cy-py)^2) + (cz-pz)^2 < r r, provided the cell
+// is static fluid (flags & fluid_bits, or no flags at all).
+__global__ void k_map_spheres(int ncx, int ncy, int ncz, const double* __restrict__ frame,
+                              const int* __restrict__ first, const double* __restrict__ spheres,
+                              const int64_t* __restrict__ uids, const uint32_t* __restrict__ flags,
+                              uint32_t fluid_bits, int64_t* __restrict__ owner) {
+    const int X = ncx + 2, Y = ncy + 2, Z = ncz + 2;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const int b = blockIdx.z / Z;
+    const int k = blockIdx.z % Z;
+    if (i >= X) return;
+    const int64_t cell = (((int64_t)b * Z + k) * Y + j) * X + i;
+    const double* fr = frame + 6 * b;
+    const double x = fr[0] + fr[3] * (double)(i - 1);
+    const double y = fr[1] + fr[4] * (double)(j - 1);
+    const double z = fr[2] + fr[5] * (double)(k - 1);
+    int64_t who = -1;
+    for (int s = first[b]; s < first[b + 1]; ++s) {
+        const double* sp = spheres + 4 * s;
+        const double r = sp[3];
+        if (!(x >= sp[0] - r && x < sp[0] + r && y >= sp[1] - r && y < sp[1] + r &&
+              z >= sp[2] - r && z < sp[2] + r))
+            continue;
+        const double ex = x - sp[0], ey = y - sp[1], ez = z - sp[2];
+        if ((ex * ex + ey * ey) + ez * ez < r * r) {
+            who = uids[s];
+            break;
+        }
+    }
+    if (who >= 0 && flags && (flags[cell] & fluid_bits) == 0u) who = -1;
+    owner[cell] = who;
+}
+
 // Sweep-time fluid mask (lbm/sweep.py:124-136): links stay as frozen at
 // freeze() (boundary.py:128-131), the collision mask follows the CURRENT
 // flags; err[0] = first unflagged interior cell + 1.
@@ -777,6 +815,24 @@ int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags, const uint32_
         return cudaGetLastError();
     });
     return cuda_status(e, "lbm_build_cellmask");
+}
+
+int lbm_map_spheres(int n_blocks, const int32_t cells[3], const double* frame, const int32_t* first,
+                    const double* spheres, const int64_t* uids, const uint32_t* flags,
+                    uint32_t fluid_bits, int64_t* owner, void* stream) {
+    if (n_blocks < 0 || !cells || cells[0] < 1 || cells[1] < 1 || cells[2] < 1)
+        return fail(LBM_EINVAL, "bad block geometry");
+    if (n_blocks == 0) return LBM_OK;
+    if (!frame || !first || !owner) return fail(LBM_EINVAL, "NULL buffer");
+    const int X = cells[0] + 2, Y = cells[1] + 2, Z = cells[2] + 2;
+    if (Y > 65535 || (int64_t)Z * n_blocks > 65535)
+        return fail(LBM_EINVAL, "block grid too large for one launch");
+    cudaStream_t s = (cudaStream_t)stream;
+    dim3 blk = cell_block(X);
+    dim3 grid((X + blk.x - 1) / blk.x, Y, Z * n_blocks);
+    k_map_spheres<<<grid, blk, 0, s>>>(cells[0], cells[1], cells[2], frame, first, spheres, uids,
+                                       flags, fluid_bits, owner);
+    return cuda_status(cudaGetLastError(), "lbm_map_spheres");
 }
 
 int lbm_refresh_fluid_mask(const lbm_grid_t* g, const uint32_t* flags, const uint32_t bits[5],

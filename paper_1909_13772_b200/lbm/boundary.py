@@ -20,26 +20,24 @@ from ..errors import ValidationError
 from ..field import FlagFieldHandler, GhostPackInfo, exchange_ghosts
 from .stencil import Stencil
 
-FLUID = "Fluid"
-NO_SLIP = "NoSlip"
-UBB = "UBB"
-PRESSURE = "Pressure"
-SOLID = "Solid"
-BOUNDARY_FLAGS = (FLUID, NO_SLIP, UBB, PRESSURE, SOLID)
-_LINK_FLAGS = (NO_SLIP, UBB, PRESSURE)
+# the five canonical flag names, in registration order
+BOUNDARY_FLAGS = FLUID, NO_SLIP, UBB, PRESSURE, SOLID = ("Fluid", "NoSlip", "UBB", "Pressure",
+                                                         "Solid")
+_LINK_FLAGS = BOUNDARY_FLAGS[1:4]     # flags a fluid cell bounces back from
 
 
-def ensure_flags(forest, flags="flags", ghost_layers=1) -> FlagFieldHandler:
-    """Register the flag slot if needed and the canonical flag names
-    (boundary.py:35-45)."""
-    if flags not in forest.handlers:
-        forest.register_data(flags, FlagFieldHandler(ghost_layers))
-    handler = forest.handlers[flags]
-    if not isinstance(handler, FlagFieldHandler):
-        raise ValidationError(f"data slot {flags!r} is not a flag field")
-    for name in BOUNDARY_FLAGS:
-        if name not in handler.registry:
-            handler.register(name)
+def ensure_flags(forest, flags="flags", ghost_layers=1):
+    """The flag slot `flags` (registered on first use) with the five
+    canonical names registered in their fixed order (boundary.py:35-45):
+    on a fresh slot Fluid=1, NoSlip=2, UBB=4, Pressure=8, Solid=16."""
+    handler = forest.handlers.get(flags)
+    if handler is None:
+        handler = FlagFieldHandler(ghost_layers)
+        forest.register_data(flags, handler)
+    elif not isinstance(handler, FlagFieldHandler):
+        raise ValidationError(f"data slot {flags!r} holds no flag field")
+    for name in (n for n in BOUNDARY_FLAGS if n not in handler.registry):
+        handler.register(name)
     return handler
 
 
@@ -147,19 +145,17 @@ class BoundaryHandling:
         self.stencil = stencil
         self.flags_key = flags
         uw = tuple(float(v) for v in ubb_velocity)
-        if len(uw) == 2:
-            uw = (uw[0], uw[1], 0.0)
-        if len(uw) != 3:
+        if len(uw) not in (2, 3):
             raise ValidationError(f"wall velocity needs 2 or 3 components, got {ubb_velocity!r}")
-        self.ubb_velocity = uw
-        self.pressure_density = float(pressure_density)
-        self.reference_density = float(reference_density)
+        self.ubb_velocity = uw + (0.0,) * (3 - len(uw))
+        self.pressure_density, self.reference_density = (float(pressure_density),
+                                                         float(reference_density))
         self.handler = ensure_flags(forest, flags)
-        self._masks = None
-        self._links = None
+        self._masks = self._links = None
         self.generation = 0
 
-    def freeze(self) -> None:
+    def freeze(self):
+        """Collective: refresh the flag ghosts, then build the device masks."""
         exchange_ghosts(self.forest, [GhostPackInfo(self.flags_key)])
         self._masks = build_masks(self.forest, self.stencil, self.flags_key)
         self._flag_snapshot = self._dense_flags()
@@ -170,34 +166,30 @@ class BoundaryHandling:
         for block in self.forest.local_blocks():
             block.data[self.flags_key].touched = False
 
-    @property
-    def frozen(self) -> bool:
-        return self._masks is not None
+    frozen = property(lambda self: self._masks is not None)
 
     @property
-    def masks(self) -> Masks:
+    def masks(self):
         if self._masks is None:
-            raise ValidationError("boundary handling not frozen yet")
+            raise ValidationError("freeze() the boundary handling first")
         return self._masks
 
     @property
     def links(self):
+        """The reference's link lists, decoded from the device masks."""
         if self._links is None:
             self._links = decode_links(self.forest, self.stencil, self.masks, self.flags_key)
         return self._links
 
-    def link_count(self, block) -> int:
-        lists = self.links[block.id]
-        return sum(len(zs) for entries in lists.values() for (_, zs, _, _) in entries)
+    def link_count(self, block):
+        return sum(len(entry[1]) for per_type in self.links[block.id].values()
+                   for entry in per_type)
 
-    def known_mask(self, block) -> np.uint32:
-        registry = block.data[self.flags_key].registry
-        out = np.uint32(0)
-        for name in BOUNDARY_FLAGS:
-            out |= registry[name]
-        return out
+    def known_mask(self, block):
+        reg = block.data[self.flags_key].registry
+        return np.bitwise_or.reduce([reg[n] for n in BOUNDARY_FLAGS], initial=np.uint32(0))
 
-    def fluid_mask(self, block) -> np.uint32:
+    def fluid_mask(self, block):
         return block.data[self.flags_key].registry[FLUID]
 
     def _dense_flags(self):

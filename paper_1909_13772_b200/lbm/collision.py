@@ -24,90 +24,94 @@ from .stencil import Stencil, basis_inverse, moment_basis, raw_moment_basis
 MAGIC_DEFAULT = Fraction(3, 16)
 
 
-def _check_rate(label, value):
+def _rate(label, value):
+    """A relaxation rate, validated in the open interval (0, 2)."""
     v = float(value)
-    if not 0.0 < v < 2.0:
-        raise ValidationError(f"{label} must lie in (0, 2), got {value}")
-    return v
+    if 0.0 < v < 2.0:
+        return v
+    raise ValidationError(f"{label} must lie in (0, 2), got {value}")
 
 
-def _force_vector(force):
-    f = tuple(float(x) for x in force)
-    if len(f) == 2:
-        f = (f[0], f[1], 0.0)
-    if len(f) != 3:
-        raise ValidationError(f"force needs 2 or 3 components, got {force!r}")
-    return f
+def _vector3(value, what="force"):
+    """2 or 3 components -> a 3-tuple of floats (a 2D vector gets z = 0)."""
+    v = tuple(map(float, value))
+    if len(v) in (2, 3):
+        return v + (0.0,) * (3 - len(v))
+    raise ValidationError(f"{what} needs 2 or 3 components, got {value!r}")
 
 
-class SRT:
-    """Single-rate collision: one global rate or a per-cell rate field."""
+class _Described:
+    """repr() from the attributes listed in `_shown`."""
 
-    mode = 0
-
-    def __init__(self, omega=None, *, omega_field=None):
-        if (omega is None) == (omega_field is None):
-            raise ValidationError("SRT needs omega or omega_field")
-        self.omega = None if omega is None else _check_rate("omega", omega)
-        self.omega_field = omega_field
+    _shown = ()
 
     def __repr__(self):
-        if self.omega_field is not None:
-            return f"SRT(omega_field={self.omega_field!r})"
-        return f"SRT(omega={self.omega})"
+        body = ", ".join(f"{k}={getattr(self, k)!r}" for k in self._shown
+                         if getattr(self, k) is not None)
+        return f"{type(self).__name__}({body})"
 
 
-class TRT:
-    """Two-rate collision (even/odd populations)."""
+class SRT(_Described):
+    """Single relaxation rate: one global omega, or omega_field = the name
+    of a per-cell rate field (read on every sweep)."""
+
+    mode = 0
+    _shown = ("omega", "omega_field")
+
+    def __init__(self, omega=None, *, omega_field=None):
+        if (omega is None) is (omega_field is None):
+            raise ValidationError("SRT takes exactly one of omega and omega_field")
+        self.omega = _rate("omega", omega) if omega is not None else None
+        self.omega_field = omega_field
+
+
+class TRT(_Described):
+    """Two relaxation rates: even (omega_e) and odd (omega_o) parts."""
 
     mode = 1
     omega_field = None
+    _shown = ("omega_e", "omega_o")
 
     def __init__(self, omega_e, omega_o):
-        self.omega_e = _check_rate("omega_e", omega_e)
-        self.omega_o = _check_rate("omega_o", omega_o)
+        self.omega_e, self.omega_o = _rate("omega_e", omega_e), _rate("omega_o", omega_o)
 
     @classmethod
     def with_magic(cls, omega_e, magic=MAGIC_DEFAULT):
-        omega_e = _check_rate("omega_e", omega_e)
-        lam_e = 1.0 / omega_e - 0.5
-        if lam_e <= 0.0:
+        """omega_o from the magic parameter Lambda = (1/omega_e - 1/2)(1/omega_o - 1/2)."""
+        we = _rate("omega_e", omega_e)
+        lam_e = 1.0 / we - 0.5
+        if not lam_e > 0.0:
             raise ValidationError("omega_e = 2 leaves the magic value undefined")
-        return cls(omega_e, 1.0 / (float(magic) / lam_e + 0.5))
+        return cls(we, 1.0 / (float(magic) / lam_e + 0.5))
 
     @property
     def magic(self):
         return (1.0 / self.omega_e - 0.5) * (1.0 / self.omega_o - 0.5)
 
-    def __repr__(self):
-        return f"TRT(omega_e={self.omega_e}, omega_o={self.omega_o})"
 
-
-class MRT:
-    """Moment-space relaxation, one rate per moment of the stencil's basis.
-
-    `basis=` (B200 extension) supplies an explicit invertible q x q moment
-    matrix, which is how D3Q27 MRT is expressed (the reference's
-    moment_basis rejects D3Q27); M^-1 is then np.linalg.inv(basis)."""
+class MRT(_Described):
+    """One relaxation rate per moment of a q x q basis: the stencil's
+    Gram-Schmidt basis (M^-1 = M^T diag(1/|m|^2)), or an explicit invertible
+    `basis=` (B200 extension; M^-1 = inv(basis)), which is how D3Q27 MRT is
+    expressed - the reference's moment_basis rejects D3Q27."""
 
     mode = 2
     omega_field = None
 
-    def __init__(self, stencil: Stencil, rates, *, basis=None):
+    def __init__(self, stencil, rates, *, basis=None):
         self.stencil = stencil
         if basis is None:
-            self.M = moment_basis(stencil).astype(np.float64)
-            self.Minv = basis_inverse(moment_basis(stencil))
+            ints = moment_basis(stencil)
+            self.M, self.Minv = ints.astype(np.float64), basis_inverse(ints)
         else:
-            M = np.asarray(basis, dtype=np.float64)
-            if M.shape != (stencil.q, stencil.q):
+            self.M = np.asarray(basis, dtype=np.float64)
+            if self.M.shape != (stencil.q, stencil.q):
                 raise ValidationError(f"basis must be {stencil.q}x{stencil.q}")
-            self.M = M
-            self.Minv = np.linalg.inv(M)
-        rates = [_check_rate(f"rate[{k}]", r) for k, r in enumerate(rates)]
-        if len(rates) != stencil.q:
-            raise ValidationError(f"{stencil.name} needs {stencil.q} rates, got {len(rates)}")
-        self.S = np.array(rates)
+            self.Minv = np.linalg.inv(self.M)
+        checked = [_rate(f"rate[{k}]", r) for k, r in enumerate(rates)]
+        if len(checked) != stencil.q:
+            raise ValidationError(f"{stencil.name} takes {stencil.q} rates, got {len(checked)}")
+        self.S = np.array(checked)
 
     @classmethod
     def uniform(cls, stencil, omega):
@@ -115,40 +119,33 @@ class MRT:
 
     @classmethod
     def raw_moments(cls, stencil, shear, other=1.0):
-        """D3Q27 raw-moment MRT: shear rows (4..8) relax at `shear`, all
-        others at `other` (BASELINE config 2: shear 1.9, others 1.0)."""
-        M = raw_moment_basis(stencil)
-        rates = [other] * stencil.q
-        for k in range(4, 9):
-            rates[k] = shear
-        return cls(stencil, rates, basis=M)
+        """D3Q27 raw-moment MRT: the shear rows 4..8 relax at `shear`, all
+        others at `other` (BASELINE config 2: 1.9 / 1.0)."""
+        rates = [shear if 4 <= k <= 8 else other for k in range(stencil.q)]
+        return cls(stencil, rates, basis=raw_moment_basis(stencil))
 
     def __repr__(self):
         return f"MRT({self.stencil.name}, rates={self.S.tolist()})"
 
 
-class Guo:
+class Guo(_Described):
     """Body force: half-shifted equilibrium velocity + relaxed source term."""
 
     mode = 1
+    _shown = ("force",)
 
     def __init__(self, force):
-        self.force = _force_vector(force)
-
-    def __repr__(self):
-        return f"Guo({self.force})"
+        self.force = _vector3(force)
 
 
-class SimpleShift:
+class SimpleShift(_Described):
     """Body force by shifting the equilibrium velocity by tau F / rho."""
 
     mode = 2
+    _shown = ("force",)
 
     def __init__(self, force):
-        self.force = _force_vector(force)
-
-    def __repr__(self):
-        return f"SimpleShift({self.force})"
+        self.force = _vector3(force)
 
 
 class KernelParams:

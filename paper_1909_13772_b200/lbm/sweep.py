@@ -176,34 +176,35 @@ def fill_equilibrium(pdf: PdfField, rho=1.0, velocity=(0.0, 0.0, 0.0)) -> None:
     (sweep.py:51-76).  Callables are evaluated on the host over cell-centre
     coordinates exactly as the reference does; the equilibrium itself is
     computed on the device straight into the HBM layout."""
-    forest = pdf.forest
     lat = pdf.lattice
-    box = lat.box
     rviews, uviews = [], []
-    for block in box.blocks:
-        field = pdf.src(block)
-        g = field.g
-        (cx0, cy0, cz0), (dx, dy, dz) = forest.cell_centers(block.id)
-        xs = cx0 + dx * (np.arange(field.nx + 2 * g) - g)
-        ys = cy0 + dy * (np.arange(field.ny + 2 * g) - g)
-        zs = cz0 + dz * (np.arange(field.nz + 2 * g) - g)
-        z, y, x = np.meshgrid(zs, ys, xs, indexing="ij")
-        r = rho(x, y, z) if callable(rho) else np.full(x.shape, float(rho))
-        r = np.broadcast_to(np.asarray(r, dtype=np.float64), x.shape)
+    for block in lat.box.blocks:
+        x, y, z = _cell_centres(pdf.forest, block.id, pdf.src(block))
+        r = rho(x, y, z) if callable(rho) else float(rho)
+        rviews.append(np.broadcast_to(np.asarray(r, dtype=np.float64), x.shape)[..., np.newaxis])
         if callable(velocity):
-            u = np.stack(np.broadcast_arrays(*velocity(x, y, z)), axis=-1)
+            comps = np.broadcast_arrays(*velocity(x, y, z))
         else:
-            u = np.broadcast_to(np.asarray(velocity, dtype=np.float64), x.shape + (len(velocity),))
-        u = np.asarray(u, dtype=np.float64)
-        if u.shape[-1] == 2:
-            u = np.concatenate([u, np.zeros(u.shape[:-1] + (1,))], axis=-1)
-        if u.shape[-1] != 3:
-            raise ValidationError(f"velocity needs 2 or 3 components, got shape {u.shape}")
-        rviews.append(r[..., None])
-        uviews.append(u)
-    rho_g = box.gather(rviews, 1, np.float64)[0]
-    u_g = np.moveaxis(box.gather(uviews, 3, np.float64), 0, 3)
+            comps = [np.full(x.shape, float(v)) for v in velocity]
+        if len(comps) not in (2, 3):
+            raise ValidationError(f"velocity needs 2 or 3 components, got {len(comps)}")
+        comps = list(comps) + [np.zeros(x.shape)] * (3 - len(comps))
+        uviews.append(np.stack([np.asarray(c, dtype=np.float64) for c in comps], axis=-1))
+    rho_g = lat.box.gather(rviews, 1, np.float64)[0]
+    u_g = np.moveaxis(lat.box.gather(uviews, 3, np.float64), 0, 3)
     lat.fill_equilibrium(rho_g, u_g)
+
+
+def _cell_centres(forest, block_id, field):
+    """(x, y, z) grids of a block's ghost-inclusive cell centres: corner
+    centre + spacing * index, index running from -g (the reference's
+    expressions, sweep.py:58-62, so callables see identical coordinates)."""
+    c0, h = forest.cell_centers(block_id)
+    g = field.g
+    axes = [c0[a] + h[a] * np.arange(-g, n + g) for a, n in enumerate((field.nx, field.ny,
+                                                                        field.nz))]
+    z, y, x = np.meshgrid(axes[2], axes[1], axes[0], indexing="ij")
+    return x, y, z
 
 
 def fill_equilibrium_arrays(pdf: PdfField, rho, u) -> None:
@@ -257,36 +258,40 @@ def macroscopic_arrays(pdf: PdfField, *, force=None, out=None):
     return (rho_t, u_t) if out is None else out
 
 
-def _require_uniform(forest) -> None:
-    for block in forest.local_blocks():
-        if block.level != 0:
-            raise TopologyError("stream-collide needs a uniform refinement level")
+def _require_uniform(forest):
+    if any(block.level != 0 for block in forest.local_blocks()):
+        raise TopologyError("stream-collide needs a uniform refinement level")
 
 
-def _prepare(pdf: PdfField, model, force, handling):
+def sweep_masks(pdf, handling):
+    """Device masks of the next sweep after the reference's checks
+    (sweep.py:97-136): one level, a handling of this stencil or a fully
+    periodic domain, one ghost layer on pdf and flags, no unflagged interior
+    cell.  A handling is frozen on first use (sweep.py:107-108)."""
     forest = pdf.forest
-    st = pdf.stencil
     _require_uniform(forest)
-    if handling is not None and handling.stencil is not st:
-        raise ValidationError("boundary handling built for a different stencil")
     if handling is None:
-        for a in range(forest.d):
-            if not forest.periodic[a]:
-                raise ValidationError("without boundary handling the domain must be fully periodic")
-    elif not handling.frozen:
-        handling.freeze()
+        if not all(forest.periodic[:forest.d]):
+            raise ValidationError("without boundary handling the domain must be fully periodic")
+    elif handling.stencil is not pdf.stencil:
+        raise ValidationError("boundary handling built for a different stencil")
     if pdf.g != 1:
         raise ValidationError("stream-collide needs exactly one pdf ghost layer")
+    if handling is None:
+        return pdf.lattice.default_masks()
+    if not handling.frozen:
+        handling.freeze()
+    if any(b.data[handling.flags_key].g != pdf.g for b in forest.local_blocks()):
+        raise ValidationError("flag and pdf ghost layers differ")
+    masks = handling.sweep_masks()
+    if masks.unflagged_cell is not None:
+        raise ValidationError(f"unflagged cell {masks.unflagged_cell}")
+    return masks
+
+
+def _prepare(pdf, model, force, handling):
+    masks = sweep_masks(pdf, handling)
     lat = pdf.lattice
-    if handling is not None:
-        for block in forest.local_blocks():
-            if block.data[handling.flags_key].g != pdf.g:
-                raise ValidationError("flag and pdf ghost layers differ")
-        masks = handling.sweep_masks()
-        if masks.unflagged_cell is not None:
-            raise ValidationError(f"unflagged cell {masks.unflagged_cell}")
-    else:
-        masks = lat.default_masks()
     kp, key = pdf.params(model, force, handling)
     key = key + (id(masks),)
     omega_key = getattr(model, "omega_field", None)
@@ -304,15 +309,14 @@ def _upload_rates(lat, omega_key):
     host values changed; returns the content version (a change re-collides
     the stored state, as the reference collides with the current rates)."""
     box = lat.box
-    dense = np.empty((box.nz, box.ny, box.nx), dtype=np.float64)
-    for block, (ox, oy, oz) in zip(box.blocks, box.offsets):
-        ow = block.data[omega_key]
-        win = ow.field.view[..., 0] if hasattr(ow, "field") else ow.view[..., 0]
-        inner = win[1:-1, 1:-1, 1:-1]
-        if np.any(inner <= 0.0) or np.any(inner >= 2.0):
-            raise ValidationError("per-cell rates must lie in (0, 2)")
-        dense[oz:oz + inner.shape[0], oy:oy + inner.shape[1], ox:ox + inner.shape[2]] = inner
-    return lat.set_rates(dense)
+    views = []
+    for block in box.blocks:
+        slot = block.data[omega_key]
+        views.append(getattr(slot, "field", slot).view[..., :1])
+    dense = box.gather(views, 1, np.float64)[0, 1:-1, 1:-1, 1:-1]
+    if not np.all((dense > 0.0) & (dense < 2.0)):
+        raise ValidationError("per-cell rates must lie in (0, 2)")
+    return lat.set_rates(np.ascontiguousarray(dense))
 
 
 def stream_collide(pdf: PdfField, model, *, force=None, handling=None) -> None:
@@ -346,27 +350,26 @@ def macroscopic_fields(pdf: PdfField, density="rho", velocity="vel", *, force=No
     rho_t, u_t, bad = lat.moments(kp, masks)
     if int(bad.item()):
         raise NumericsError(f"non-positive density {float(rho_t.min().item())}")
-    rho = rho_t.cpu().numpy()
-    u = u_t.cpu().numpy()
-    box = lat.box
-    for block, (ox, oy, oz) in zip(box.blocks, box.offsets):
-        n = forest.cells_per_block
-        sl = (slice(oz, oz + n[2]), slice(oy, oy + n[1]), slice(ox, ox + n[0]))
+    rho, u = rho_t.cpu().numpy(), u_t.cpu().numpy()
+    cpb = forest.cells_per_block
+    for block, off in zip(lat.box.blocks, lat.box.offsets):
+        window = tuple(slice(off[a], off[a] + cpb[a]) for a in (2, 1, 0))
+        keep = np.ones(tuple(cpb[::-1]), dtype=bool)
         if handling is not None:
-            flags = block.data[handling.flags_key]
-            fluid = (flags.field.interior[..., 0] & handling.fluid_mask(block)) != 0
-        else:
-            fluid = slice(None)
+            bits = block.data[handling.flags_key].field.interior[..., 0]
+            keep = (bits & handling.fluid_mask(block)) != 0
         if density is not None:
-            block.data[density].interior[..., 0][fluid] = rho[sl][fluid]
+            dst = block.data[density].interior[..., 0]
+            dst[keep] = rho[window][keep]
         if velocity is not None:
-            out = block.data[velocity].interior
-            for a in range(out.shape[-1]):
-                out[..., a][fluid] = u[sl][..., a][fluid]
+            dst = block.data[velocity].interior
+            src = u[window][..., :dst.shape[-1]]
+            dst[keep] = src[keep]
 
 
-def mlups(interior_cells, steps, seconds) -> float:
-    """Million lattice-cell updates per second (sweep.py:179-183)."""
-    if seconds <= 0.0:
-        raise ValidationError(f"need a positive wall time, got {seconds}")
+def mlups(interior_cells, steps, seconds):
+    """Million lattice-cell updates per second (sweep.py:179-183): every
+    interior cell counts, solid ones included."""
+    if not seconds > 0.0:
+        raise ValidationError(f"mlups needs a positive wall time, got {seconds}")
     return interior_cells * steps / seconds / 1.0e6
