@@ -12,7 +12,7 @@ HBM over NVLink, CUDA IPC); NCCL send/recv of the contiguous runs is the
 fallback transport (halo.py).
 """
 from .errors import BackendError, BlocksimError, BufferUnderflowError, NumericsError, \
-    SyncError, TopologyError, TypeTagError, ValidationError
+    SyncError, TopologyError, TypeTagError, UnrecoverableError, ValidationError
 from .runtime import Context, ThreadContext, init_distributed, run
 from .blockforest import BlockForest, BlockId, create_forest
 from .field import Field, FieldDataHandler, FlagField, FlagFieldHandler, GhostPackInfo, \
@@ -23,6 +23,7 @@ from .vtk import write_block_vtk, write_vtk
 from .wire import RecvBuffer, SendBuffer
 from .bodies import BodyStorage, BodyStorageHandler, RigidBody, Sphere, add_sphere, find_body, \
     ghost_bodies, local_bodies, register_bodies, sync_bodies
+from .checkpoint import BuddyCheckpoint
 from .coupling import CoupledSystem, ParticleMapping, coupled_time_step, covered_cell_counts, \
     map_bodies, moving_boundary_sweep, reduce_hydrodynamic_forces, reinitialize_uncovered
 

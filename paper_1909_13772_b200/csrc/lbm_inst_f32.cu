@@ -90,10 +90,12 @@ cudaError_t set_mrt_fast_f32(int q, const double* tables, cudaStream_t s, int* f
                 if (fabs(H[a][b] - ((a == b ? 1.0 : 0.0) - 0.5 * K[a][b])) > tol) { ok = 0; break; }
     }
     if (ok) {
+        // the kernel applies I - K (lbm_collide_f32.cuh, factorised MRT)
         float kd[27], kb[9];
-        for (int r = 0; r < 27; ++r) kd[r] = (float)K[r][r];
+        for (int r = 0; r < 27; ++r) kd[r] = (float)(1.0 - K[r][r]);
         for (int a = 0; a < 3; ++a)
-            for (int b = 0; b < 3; ++b) kb[a * 3 + b] = (float)K[blk[a]][blk[b]];
+            for (int b = 0; b < 3; ++b)
+                kb[a * 3 + b] = (float)((a == b ? 1.0 : 0.0) - K[blk[a]][blk[b]]);
         cudaError_t e;
         if ((e = cudaMemcpyToSymbolAsync(c_mrt_kd, kd, sizeof(kd), 0, cudaMemcpyHostToDevice, s)) !=
             cudaSuccess)

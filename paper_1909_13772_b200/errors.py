@@ -36,3 +36,7 @@ class BufferUnderflowError(BlocksimError):
 class BackendError(BlocksimError):
     """The CUDA kernel library is missing or a launch failed.  There is no
     CPU fallback: every compute call goes through the sm_100a library."""
+
+
+class UnrecoverableError(BlocksimError):
+    """A checkpoint cannot restore the lost state (errors.py:48)."""

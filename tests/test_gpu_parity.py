@@ -176,6 +176,20 @@ def test_fp32_storage_within_1e5_relative(api, spec_name):
     assert rel < TOL_F32_REL, rel
 
 
+@pytest.mark.parametrize("force", [None, ("Guo", (2e-5, -1e-5, 3e-6)), ("Guo", (3e-5, 0.0, 0.0))])
+def test_fp32_factorised_d3q27_mrt_with_and_without_guo(api, force):
+    """The fp32 D3Q27 raw-moment MRT (moment-space form without force, the
+    population-space form with Guo) against the fp64 oracle, 1e-5 relative."""
+    spec = dict(stencil="D3Q27", dims=(24, 20, 22), root_dims=(1, 1, 1),
+                periodic=(True, True, True), geometry=None, model=("MRT_raw", 1.9, 1.0),
+                force=force, init=("random", 13), steps=150, snapshots=(150,), layout="fzyx")
+    res = cases.run_case(api, _ctx(), spec, pdf_kwargs={"dtype": "float32"})
+    ores = cases.oracle_run(spec, oracle)
+    a, b = res["pdf"][150], ores["pdf"][150]
+    rel = float(np.max(np.abs(a - b) / np.abs(b)))
+    assert rel < TOL_F32_REL, rel
+
+
 @pytest.mark.parametrize("name", ["c1_trt_guo_porous", "c2_d3q27_trt_cavity", "d2q9_pressure_box",
                                   "d3q19_shift_ghostwalls"])
 def test_link_sets_equal_exhaustive_scan(api, name):
