@@ -203,7 +203,10 @@ int lbm_face_span(const lbm_grid_t* g, int face, int64_t* send_off,
  * typemask: (nz, ny, nx, 2) uint32 - word 0 UBB link bits, word 1 Pressure
  * link bits - only read where LBM_MASK_UBB / LBM_MASK_PRESSURE is set.
  * cellmask = typemask = NULL: every cell is fluid and has no link (a
- * periodic domain without boundary handling); no mask bytes are read. */
+ * periodic domain without boundary handling); no mask bytes are read.
+ * typemask = NULL with a cellmask: no cell carries LBM_MASK_UBB /
+ * LBM_MASK_PRESSURE (NoSlip-only links); the typed corrections are compiled
+ * out of the launched kernel (ABI 5). */
 int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p,
                    const void* src, void* dst, const uint32_t* cellmask,
                    const uint32_t* typemask, int z_begin, int z_end,

@@ -553,7 +553,7 @@ int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p, const void* src, 
     int st = check_grid(g, &k);
     if (st != LBM_OK) return st;
     if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
-    if (!src || !dst || (cellmask && !typemask)) return fail(LBM_EINVAL, "NULL buffer");
+    if (!src || !dst) return fail(LBM_EINVAL, "NULL buffer");
     if (src == dst) return fail(LBM_EINVAL, "fused step needs two fields (src != dst)");
     if (z_begin < 0 || z_end > g->nz || z_begin > z_end)
         return fail(LBM_EINVAL, "plane range [%d, %d) outside 0..%d", z_begin, z_end, g->nz);
@@ -574,7 +574,7 @@ int lbm_fused_step_peer(const lbm_grid_t* g, const lbm_params_t* p, const void* 
     int st = check_grid(g, &k);
     if (st != LBM_OK) return st;
     if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
-    if (!src || !dst || (cellmask && !typemask)) return fail(LBM_EINVAL, "NULL buffer");
+    if (!src || !dst) return fail(LBM_EINVAL, "NULL buffer");
     if (src == dst) return fail(LBM_EINVAL, "fused step needs two fields (src != dst)");
     if (z_begin < 0 || z_end > g->nz || z_begin > z_end)
         return fail(LBM_EINVAL, "plane range [%d, %d) outside 0..%d", z_begin, z_end, g->nz);

@@ -27,6 +27,11 @@ inline dim3 cell_block(int nx) {
     return dim3(bx, 1, 1);
 }
 
+inline bool use_z2() {
+    const char* e = getenv("LBM_B200_Z2");
+    return !(e && e[0] == '0');
+}
+
 inline dim3 fused_block(int nx) {
     int bx = nx >= LBM_FUSED_BX ? LBM_FUSED_BX : ((nx + 31) / 32) * 32;
     return dim3(bx, 1, 1);
@@ -183,6 +188,18 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
     dim3 b = fused_block(g.nx);
     dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
     const bool peer = p.peer_lo != nullptr || p.peer_hi != nullptr;
+    // fp32 D3Q19 SRT / TRT without typed (UBB / Pressure) links: two cells
+    // per thread along z (k_fused_z2, spill-free at 80 registers; the typed
+    // corrections' register demand would make it spill, so typed launches
+    // keep k_fused).  LBM_B200_Z2=0 selects k_fused (A/B runs).
+    if constexpr (std::is_same_v<LBM_REAL, float> && Q == 19 && (MODEL == 0 || MODEL == 1)) {
+        if (!p.mv_link && !peer && !tmk && use_z2()) {
+            dim3 grid2(grid.x, grid.y, (z1 - z0 + 1) / 2);
+            k_fused_z2<Q, LBM_REAL, MODEL, FORCE, false><<<grid2, b, 0, s>>>(
+                g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0, z1);
+            return cudaGetLastError();
+        }
+    }
     if (p.mv_link) {
         // moving-body walls: a separate instantiation, so the standard sweep
         // keeps its register allocation (3D stencils, SRT/TRT/dense MRT)

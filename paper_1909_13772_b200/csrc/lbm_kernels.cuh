@@ -260,7 +260,7 @@ __device__ __forceinline__ void moving_links(const KGrid& g, const KParams& p, i
     }
 }
 
-template <int Q, typename Real, typename Acc, int MV>
+template <int Q, typename Real, typename Acc, int MV, bool TYPED = true>
 __device__ __forceinline__ void pull_finish(const KGrid& g, const KParams& p,
                                             const Real* __restrict__ src, int x, int y, int z,
                                             int64_t own, uint32_t code, uint2 t, const Real (&raw)[Q],
@@ -309,18 +309,14 @@ __device__ __forceinline__ void pull_offsets(const KGrid& g, int x, int y, int z
 // Acc = float (fp32 storage only): the stored centred g = f - w as is.
 // MV: 0 no moving-body walls (the standard sweep kernels), 1 moving walls
 // without force accumulation (readouts), 2 moving walls + forces (fused step).
-template <int Q, typename Real, typename Acc, int MV = 0>
-__device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
-                                          const Real* __restrict__ src, int x, int y, int z,
-                                          uint32_t code, const uint32_t* __restrict__ typemask,
-                                          bool generic, Acc (&f)[Q]) {
-    static_assert(std::is_same_v<Acc, double> || std::is_same_v<Real, float>,
-                  "fp32 registers only for fp32 storage");
+// Phases 1 + 2 of a pull: source offsets (link substitution as a select)
+// and all Q loads in flight.
+template <int Q, typename Real>
+__device__ __forceinline__ void pull_load(const KGrid& g, const Real* __restrict__ src, int x,
+                                          int y, int z, uint32_t code, bool generic,
+                                          Real (&raw)[Q]) {
     using D = Dirs<Q>;
     const int64_t own = lidx(g, z, 0, y, x);
-    uint2 t = make_uint2(0u, 0u);
-    if (code & (LBM_MASK_UBB | LBM_MASK_PRESSURE)) t = __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
-    Real raw[Q];
     // link: read the own cell's direction k = opp(i) instead (w_k == w_i, so
     // the fp32 zero-centring offset is the same)
     if (!generic) {
@@ -359,12 +355,33 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
             raw[i] = __ldg(src + off[i]);
         });
     }
-    pull_finish<Q, Real, Acc, MV>(g, p, src, x, y, z, own, code, t, raw, f);
+}
+
+// typed-link words of a cell (read only where the cell has UBB / Pressure links)
+__device__ __forceinline__ uint2 type_words(const KGrid& g, const uint32_t* __restrict__ typemask,
+                                            int x, int y, int z, uint32_t code) {
+    if (!(code & (LBM_MASK_UBB | LBM_MASK_PRESSURE))) return make_uint2(0u, 0u);
+    return __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
+}
+
+template <int Q, typename Real, typename Acc, int MV = 0>
+__device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
+                                          const Real* __restrict__ src, int x, int y, int z,
+                                          uint32_t code, const uint32_t* __restrict__ typemask,
+                                          bool generic, Acc (&f)[Q]) {
+    static_assert(std::is_same_v<Acc, double> || std::is_same_v<Real, float>,
+                  "fp32 registers only for fp32 storage");
+    const uint2 t = type_words(g, typemask, x, y, z, code);
+    Real raw[Q];
+    pull_load<Q, Real>(g, src, x, y, z, code, generic, raw);
+    pull_finish<Q, Real, Acc, MV>(g, p, src, x, y, z, lidx(g, z, 0, y, x), code, t, raw, f);
 }
 
 // Phase 3 of a pull: widen the raw pulled values and apply the rare UBB /
 // Pressure / moving-wall corrections (shared by the LDG and TMA kernels).
-template <int Q, typename Real, typename Acc, int MV>
+// TYPED = false compiles the corrections out (launches whose masks carry no
+// UBB / Pressure link, where no typemask exists).
+template <int Q, typename Real, typename Acc, int MV, bool TYPED>
 __device__ __forceinline__ void pull_finish(const KGrid& g, const KParams& p,
                                             const Real* __restrict__ src, int x, int y, int z,
                                             int64_t own, uint32_t code, uint2 t, const Real (&raw)[Q],
@@ -377,7 +394,7 @@ __device__ __forceinline__ void pull_finish(const KGrid& g, const KParams& p,
         if constexpr (std::is_same_v<Acc, double>) f[i] = Store<Real>::template widen<Q, i>(raw[i]);
         else f[i] = raw[i];
     });
-    if (typed) {
+    if (TYPED && typed) {
         if (t.x) {
             static_for<1, Q>([&](auto I_) {
                 constexpr int i = decltype(I_)::value;
@@ -522,6 +539,65 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FO
         });
     }
     }
+}
+
+// Two cells per thread, stacked in z (fp32 storage): both cells' 2Q pulls
+// are issued before the first cell is finished, so each warp keeps twice the
+// bytes in flight of k_fused with far fewer than twice the registers (the
+// fp32 populations take one register each).  The kernel is latency-bound on
+// its pulls (ncu: long_scoreboard dominates), so more loads in flight per
+// resident warp is the lever; the collision and stores of cell a overlap
+// the tail of cell b's loads.  Plane pairs [z0 + 2k, z0 + 2k + 1] per block
+// row; an odd range's last plane runs alone.
+template <int Q, typename Real, int MODEL, int FORCE>
+constexpr int fused_z2_minb() {
+#ifdef LBM_FUSED_Z2_MINB
+    return LBM_FUSED_Z2_MINB;
+#else
+    return 6;
+#endif
+}
+
+__device__ __forceinline__ bool plane_wraps(const KGrid& g, int z) {
+    return (g.zlo == LBM_ZFACE_WRAP && z == 0) || (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1);
+}
+
+template <int Q, typename Real, int MODEL, int FORCE, bool TYPED>
+__global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FORCE>())
+    k_fused_z2(KGrid g, KParams p, const Real* __restrict__ src, Real* __restrict__ dst,
+               const uint32_t* __restrict__ cellmask, const uint32_t* __restrict__ typemask,
+               int z0, int z1) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int za = z0 + 2 * blockIdx.z;
+    const bool two = za + 1 < z1;                      // block-uniform
+    const int xw0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    const bool edge_xy = (g.wrap_x && (xw0 == 0 || xw0 + 32 >= g.nx)) ||
+                         (g.wrap_y && (y == 0 || y == g.ny - 1));
+    if (x >= g.nx) return;
+    const int64_t plane_cells = (int64_t)g.ny * g.nx;
+    const int64_t cell_a = ((int64_t)za * g.ny + y) * g.nx + x;
+    const uint32_t code_a = cellmask ? __ldg(cellmask + cell_a) : LBM_MASK_FLUID;
+    const uint32_t code_b = !two ? 0u : cellmask ? __ldg(cellmask + cell_a + plane_cells)
+                                                 : LBM_MASK_FLUID;
+    using Acc = AccOf<Real>;
+    Real ra[Q], rb[Q];
+    pull_load<Q, Real>(g, src, x, y, za, code_a, edge_xy || plane_wraps(g, za), ra);
+    if (two) pull_load<Q, Real>(g, src, x, y, za + 1, code_b, edge_xy || plane_wraps(g, za + 1), rb);
+    auto finish = [&](int z, int64_t cell, uint32_t code, const Real (&raw)[Q]) {
+        Acc f[Q];
+        const uint2 t = TYPED ? type_words(g, typemask, x, y, z, code) : make_uint2(0u, 0u);
+        pull_finish<Q, Real, Acc, 0, TYPED>(g, p, src, x, y, z, lidx(g, z, 0, y, x), code, t, raw,
+                                            f);
+        if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p, cell);
+        Real* dp = opaque(dst + lidx(g, z, 0, y, x));
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            store_any<Q, i>(dp + g.dslot[i], f[i]);
+        });
+    };
+    finish(za, cell_a, code_a, ra);
+    if (two) finish(za + 1, cell_a + plane_cells, code_b, rb);
 }
 
 // G_0 = C(R_0): collide fluid interior cells in place.

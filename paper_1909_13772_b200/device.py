@@ -134,6 +134,12 @@ class Masks:
         self.unflagged_cell = unflagged_cell
         self.all_fluid = all_fluid    # the fused step may skip the mask (NULL)
 
+    @property
+    def typed(self) -> bool:
+        """Some cell has a UBB or Pressure link (the fused step needs the
+        typemask; without any it gets NULL and the corrections compile out)."""
+        return bool(self.counts.get("UBB", 0) or self.counts.get("Pressure", 0))
+
 
 def all_fluid_masks(box: RankBox, device) -> Masks:
     cm = torch.full((box.nz, box.ny, box.nx), _lib.MASK_FLUID, dtype=torch.int32, device=device)
@@ -432,7 +438,8 @@ class DeviceLattice:
         if masks.all_fluid:
             cm = tm = None      # fused step reads no mask bytes
         else:
-            cm, tm = _lib.ptr(masks.cellmask), _lib.ptr(masks.typemask)
+            cm = _lib.ptr(masks.cellmask)
+            tm = _lib.ptr(masks.typemask) if masks.typed else None
         lib = _lib.load()
         main = self.stream
         if self.has_halo:
