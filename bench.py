@@ -483,9 +483,31 @@ def run_e2e(args, cfg, ctx, dtype, P, forest, pdf, handling, model, force, dims)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
     cells = nx * ny * nz
+    # where the time goes (an untimed replay of the same job, each phase
+    # between synchronisations; no nsys in this image)
+    phases = {}
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    P.fill_equilibrium_arrays(pdf, rho_h, u_h)
+    torch.cuda.synchronize()
+    phases["h2d_fill_ms"] = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        P.stream_collide(pdf, model, force=force, handling=handling)
+    torch.cuda.synchronize()
+    phases["sweeps_ms"] = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    P.macroscopic_arrays(pdf, force=force, out=out)
+    torch.cuda.synchronize()
+    phases["moments_d2h_ms"] = (time.perf_counter() - t) * 1e3
+    moved = cells * 32
+    phases["h2d_gbs"] = moved / (phases["h2d_fill_ms"] * 1e6)
+    phases["d2h_gbs"] = moved / (phases["moments_d2h_ms"] * 1e6)
     return {"value": round(cells * ctx.n_ranks * args.steps / dt / 1e6, 1), "unit": "MLUPS",
             "h2d_bytes_per_step": int(cells * 32 / args.steps),
             "d2h_bytes_per_step": int(cells * 32 / args.steps),
+            "seconds": round(dt, 4),
+            "breakdown": {k: round(v, 2) for k, v in phases.items()},
             "timed": "H2D rho/u (pinned) + fill_equilibrium_arrays + K x stream_collide + "
                      "macroscopic_arrays D2H (pinned), wall clock, max over ranks, after one "
                      "untimed pass of the same job"}

@@ -342,6 +342,12 @@ int lbm_macroscopic_cells(int q, const lbm_params_t* p, const double* f,
                           double* rho, double* u, int* bad_count, int64_t n,
                           void* stream);
 
+/* Copy the ghost shell (every q slot of every ghost cell: z ghost planes,
+ * y ghost rows and x ghost columns of the interior planes) of one field to
+ * another (ABI 5).  The second field of a fresh G_0 needs only this: its
+ * interior is written by the first fused step. */
+int lbm_copy_shell(const lbm_grid_t* g, const void* src, void* dst, void* stream);
+
 /* Validate (g, p) and make the current device hold p's constant-memory
  * state (MRT tables; uploaded on `stream` only when the device holds other
  * content).  Every launch entry point does this itself; call it before

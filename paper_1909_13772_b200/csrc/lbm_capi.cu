@@ -358,6 +358,38 @@ __global__ void k_map_spheres(int ncx, int ncy, int ncz, const double* __restric
     owner[cell] = who;
 }
 
+// Ghost shell copy (all q slots of every ghost cell of the box: the two
+// z ghost planes, and the y ghost rows / x ghost columns of each interior
+// plane).  Element type T = the storage word (8 or 4 bytes).
+template <typename T>
+__global__ void k_copy_shell(KGrid g, int q, const T* __restrict__ src, T* __restrict__ dst) {
+    const int X = g.nx + 2, Y = g.ny + 2;
+    const int zg = blockIdx.z;                       // ghost-inclusive plane
+    const int slot = blockIdx.y;
+    const bool ghost_plane = zg == 0 || zg == g.nz + 1;
+    // a ghost plane copies all Y rows; an interior plane its 2 ghost rows
+    // (y = 0, Y-1, full width) and 2 ghost columns (x = 0, X-1, Y-2 rows)
+    const int64_t n = ghost_plane ? (int64_t)X * Y : (int64_t)2 * X + 2 * (Y - 2);
+    const int64_t base = (int64_t)zg * g.zstride + (int64_t)slot * g.plane + g.xoff - 1;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int x, y;
+        if (ghost_plane) {
+            y = (int)(k / X);
+            x = (int)(k % X);
+        } else if (k < 2 * X) {
+            y = k < X ? 0 : Y - 1;
+            x = (int)(k % X);
+        } else {
+            const int r = (int)(k - 2 * X);
+            y = 1 + r / 2;
+            x = (r & 1) ? X - 1 : 0;
+        }
+        const int64_t e = base + (int64_t)y * g.pitch + x;
+        dst[e] = src[e];
+    }
+}
+
 // Sweep-time fluid mask (lbm/sweep.py:124-136): links stay as frozen at
 // freeze() (boundary.py:128-131), the collision mask follows the CURRENT
 // flags; err[0] = first unflagged interior cell + 1.
@@ -941,6 +973,21 @@ int lbm_macroscopic_cells(int q, const lbm_params_t* p, const double* f, double*
         return cudaGetLastError();
     });
     return cuda_status(e, "lbm_macroscopic_cells");
+}
+
+int lbm_copy_shell(const lbm_grid_t* g, const void* src, void* dst, void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!src || !dst) return fail(LBM_EINVAL, "NULL buffer");
+    if (src == dst) return LBM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    dim3 grid(64, g->q, g->nz + 2);
+    if (g->real_bytes == 8)
+        k_copy_shell<uint64_t><<<grid, 256, 0, s>>>(k, g->q, (const uint64_t*)src, (uint64_t*)dst);
+    else
+        k_copy_shell<uint32_t><<<grid, 256, 0, s>>>(k, g->q, (const uint32_t*)src, (uint32_t*)dst);
+    return cuda_status(cudaGetLastError(), "lbm_copy_shell");
 }
 
 int lbm_bind_params(const lbm_grid_t* g, const lbm_params_t* p, void* stream) {
