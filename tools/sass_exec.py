@@ -2,6 +2,7 @@
 """Executed-instruction mix of a kernel from an ncu report's source page.
 
     python tools/sass_exec.py gpurun_out/x.ncu-rep [--cells N] [--top K]
+    python tools/sass_exec.py gpurun_out/x_source.csv ...   (an exported source page)
 
 Groups `Instructions Executed` (warp-level) by opcode (first mnemonic
 component), prints totals per 32 cells, and the K hottest instructions by
@@ -20,10 +21,14 @@ def main():
     ap.add_argument("--cells", type=float, default=0)
     ap.add_argument("--top", type=int, default=0)
     a = ap.parse_args()
-    out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    if a.rep.endswith(".csv"):
+        out = open(a.rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source",
+                              "sass"], capture_output=True, text=True).stdout
     lines = out.splitlines()
-    rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
+    start = next(k for k, l in enumerate(lines) if l.startswith('"Address"'))
+    rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
     h = rows[0]
     ie, src, st = h.index("Instructions Executed"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
     ops, total, hot = Counter(), 0, []
