@@ -43,6 +43,7 @@
  *                       store their crossing directions into the
  *                       neighbour's ghost plane (peer HBM over NVLink);
  *                       lbm_stream_signal / lbm_stream_wait order the phases.
+ *   lbm_slot_apply_links  BoundaryHandling.apply on host views (boundary.py:154-195).
  *   lbm_slot_collide / lbm_slot_stream_pull  the kernel slot itself,
  *                       impl.collide / impl.stream_pull
  *                       (_kernels/__init__.py:10-37, _core_py.py:70-218) on
@@ -363,6 +364,16 @@ int lbm_bind_params(const lbm_grid_t* g, const lbm_params_t* p, void* stream);
 int lbm_slot_collide(int q, const lbm_params_t* p, double* f,
                      const uint32_t* flags, uint32_t fluid_bits, int64_t n,
                      void* stream);
+/* BoundaryHandling.apply (lbm/boundary.py:154-195) on dense (n, q) fp64
+ * arrays (one block's ghost-inclusive box flattened): for each of the
+ * n_links links (kind 0 NoSlip, 1 UBB, 2 Pressure; dir = the direction i
+ * from the fluid cell into the wall; cell = flat cell index),
+ * dst[cell, opp(i)] = src[cell, i] (NoSlip), src[cell, i] - p->ubb[i] (UBB),
+ * or -src[cell, i] + p->pressure[i] ((1 + 4.5 cu^2) - 1.5 u^2) with rho, u
+ * of src[cell, :] (Pressure).  All arrays are DEVICE pointers. */
+int lbm_slot_apply_links(int q, const lbm_params_t* p, const int32_t* kind,
+                         const int32_t* dir, const int64_t* cell, int64_t n_links,
+                         const double* src, double* dst, void* stream);
 /* impl.stream_pull (_core_py.py:203-218): src is a dense ghost-inclusive
  * (nzg, nyg, nxg, q) fp64 box with gl ghost layers (device); out receives
  * the interior (nzg-2gl, nyg-2gl, nxg-2gl, q) with

@@ -32,7 +32,7 @@ EXPORTS = (
     "lbm_stream_signal", "lbm_stream_wait", "lbm_copy_async",
     "lbm_ipc_export", "lbm_ipc_open", "lbm_ipc_close",
     "lbm_bind_params", "lbm_slot_collide", "lbm_slot_stream_pull", "lbm_refresh_fluid_mask",
-    "lbm_map_spheres", "lbm_copy_shell",
+    "lbm_map_spheres", "lbm_copy_shell", "lbm_slot_apply_links",
 )
 
 
@@ -116,6 +116,7 @@ def load(path: Path | None = None):
         "lbm_refresh_fluid_mask": ([G, P, P, P, P, P, P], I),
         "lbm_map_spheres": ([I, P, P, P, P, P, P, ctypes.c_uint32, P, P], I),
         "lbm_copy_shell": ([G, P, P, P], I),
+        "lbm_slot_apply_links": ([I, PR, P, P, P, I64, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -461,6 +461,52 @@ __global__ void k_slot_stream_pull(SlotStencil c, int q, const double* __restric
     }
 }
 
+// BoundaryHandling.apply (lbm/boundary.py:154-195) on dense (n, q) arrays:
+// one thread per link (kind 0 NoSlip, 1 UBB, 2 Pressure; direction i from
+// the fluid cell into the wall), dst[cell, opp(i)] from post-collision src.
+template <int Q>
+__global__ void k_apply_links(KParams p, const int32_t* __restrict__ kind,
+                              const int32_t* __restrict__ dir, const int64_t* __restrict__ cell,
+                              const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
+    using D = Dirs<Q>;
+    const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= n) return;
+    const int i = dir[l];
+    const double* s = src + cell[l] * Q;
+    double v = s[i];
+    if (kind[l] == 1) {
+        v = v - p.ubb[i];
+    } else if (kind[l] == 2) {
+        double rho = s[0];
+        for (int k = 1; k < Q; ++k) rho = rho + s[k];
+        double mx = 0.0, my = 0.0, mz = 0.0;
+        static_for<0, Q>([&](auto K_) {
+            constexpr int k = decltype(K_)::value;
+            if constexpr (D::cx[k] == 1) mx = mx + s[k];
+            if constexpr (D::cx[k] == -1) mx = mx - s[k];
+            if constexpr (D::cy[k] == 1) my = my + s[k];
+            if constexpr (D::cy[k] == -1) my = my - s[k];
+            if constexpr (D::cz[k] == 1) mz = mz + s[k];
+            if constexpr (D::cz[k] == -1) mz = mz - s[k];
+        });
+        const double ux = mx / rho, uy = my / rho, uz = mz / rho;
+        double cu = 0.0;
+        static_for<0, Q>([&](auto K_) {
+            constexpr int k = decltype(K_)::value;
+            if (k == i) cu = cu_of<Q, k>(ux, uy, uz);
+        });
+        const double usq = (ux * ux + uy * uy) + uz * uz;
+        v = -v + p.pw[i] * ((1.0 + (4.5 * cu) * cu) - 1.5 * usq);
+    }
+    int o = 0;
+    static_for<0, Q>([&](auto K_) {
+        constexpr int k = decltype(K_)::value;
+        constexpr int ok = D::opp[k];
+        if (k == i) o = ok;
+    });
+    dst[cell[l] * Q + o] = v;
+}
+
 template <int Q>
 __global__ void k_equilibrium_cells(const double* __restrict__ rho, const double* __restrict__ u,
                                     double* __restrict__ f, int64_t n) {
@@ -1035,6 +1081,32 @@ int lbm_slot_collide(int q, const lbm_params_t* p, double* f, const uint32_t* fl
         return cudaErrorInvalidValue;
     });
     return cuda_status(e, "lbm_slot_collide");
+}
+
+int lbm_slot_apply_links(int q, const lbm_params_t* p, const int32_t* kind, const int32_t* dir,
+                         const int64_t* cell, int64_t n_links, const double* src, double* dst,
+                         void* stream) {
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!q_ok(q)) return fail(LBM_EINVAL, "q must be 9, 19 or 27, got %d", q);
+    if (!p) return fail(LBM_EINVAL, "params is NULL");
+    lbm_params_t copy = *p;
+    copy.model = LBM_SRT;
+    copy.force_mode = LBM_FORCE_NONE;
+    copy.mrt = nullptr;
+    copy.moving = nullptr;
+    int st = check_params(&copy, q, &kp, s, 8);
+    if (st != LBM_OK) return st;
+    if (n_links <= 0) return LBM_OK;
+    if (!kind || !dir || !cell || !src || !dst) return fail(LBM_EINVAL, "NULL buffer");
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((n_links + threads - 1) / threads);
+    cudaError_t e = by_q(q, [&](auto Qc) {
+        k_apply_links<decltype(Qc)::value><<<blocks, threads, 0, s>>>(kp, kind, dir, cell, src, dst,
+                                                                     n_links);
+        return cudaGetLastError();
+    });
+    return cuda_status(e, "lbm_slot_apply_links");
 }
 
 int lbm_slot_stream_pull(int q, const int32_t* cx, const int32_t* cy, const int32_t* cz,

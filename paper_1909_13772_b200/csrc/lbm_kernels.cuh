@@ -309,37 +309,6 @@ __device__ __forceinline__ void pull_offsets(const KGrid& g, int x, int y, int z
 // Acc = float (fp32 storage only): the stored centred g = f - w as is.
 // MV: 0 no moving-body walls (the standard sweep kernels), 1 moving walls
 // without force accumulation (readouts), 2 moving walls + forces (fused step).
-// Early pulls (storages without the keep-in-L2 link hint, i.e. fp32): the Q
-// pulls go out before the cell mask has arrived - their addresses do not
-// depend on it - and only cells with bounce-back links then re-load those
-// directions from their own cell (slot opp(i)).  The wall-cell line a link
-// direction reads first is fetched for the neighbouring lanes anyway, and
-// the own-cell reload hits the line the wall cell's own pull brings in.
-// Removes the mask-load -> pull dependency that ncu showed as ~16 % of the
-// fp32 kernel's stall samples (R2P waiting on the mask).
-template <int Q, typename Real>
-__device__ __forceinline__ void pull_direct(const KGrid& g, const Real* __restrict__ src,
-                                            int64_t own, Real (&raw)[Q]) {
-    const Real* sp = opaque(src + own);
-    static_for<0, Q>([&](auto I_) {
-        constexpr int i = decltype(I_)::value;
-        raw[i] = __ldg(sp + g.dpull[i]);
-    });
-}
-
-template <int Q, typename Real>
-__device__ __forceinline__ void pull_links(const KGrid& g, const Real* __restrict__ src,
-                                           int64_t own, uint32_t code, Real (&raw)[Q]) {
-    constexpr uint32_t kLinks = (Q == 32 ? 0u : (1u << Q)) - 2u;   // bits 1..Q-1
-    if (code & kLinks) {
-        const Real* sp = opaque(src + own);
-        static_for<1, Q>([&](auto I_) {
-            constexpr int i = decltype(I_)::value;
-            if ((code >> i) & 1u) raw[i] = __ldg(sp + g.dlink[i]);
-        });
-    }
-}
-
 // Phases 1 + 2 of a pull: source offsets (link substitution as a select)
 // and all Q loads in flight.
 template <int Q, typename Real>
@@ -348,13 +317,6 @@ __device__ __forceinline__ void pull_load(const KGrid& g, const Real* __restrict
                                           Real (&raw)[Q]) {
     using D = Dirs<Q>;
     const int64_t own = lidx(g, z, 0, y, x);
-    if constexpr (!link_hint<Real>()) {
-        if (!generic) {
-            pull_direct<Q, Real>(g, src, own, raw);
-            pull_links<Q, Real>(g, src, own, code, raw);
-            return;
-        }
-    }
     // link: read the own cell's direction k = opp(i) instead (w_k == w_i, so
     // the fp32 zero-centring offset is the same)
     if (!generic) {
@@ -620,24 +582,8 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FO
                                                  : LBM_MASK_FLUID;
     using Acc = AccOf<Real>;
     Real ra[Q], rb[Q];
-    const bool gen_a = edge_xy || plane_wraps(g, za);
-    const bool gen_b = edge_xy || plane_wraps(g, za + 1);
-    if constexpr (!link_hint<Real>()) {
-        if (!gen_a && !gen_b) {
-            // all 2Q pulls first, then the link re-loads of both cells
-            const int64_t own_a = lidx(g, za, 0, y, x);
-            pull_direct<Q, Real>(g, src, own_a, ra);
-            if (two) pull_direct<Q, Real>(g, src, own_a + g.zstride, rb);
-            pull_links<Q, Real>(g, src, own_a, code_a, ra);
-            if (two) pull_links<Q, Real>(g, src, own_a + g.zstride, code_b, rb);
-        } else {
-            pull_load<Q, Real>(g, src, x, y, za, code_a, gen_a, ra);
-            if (two) pull_load<Q, Real>(g, src, x, y, za + 1, code_b, gen_b, rb);
-        }
-    } else {
-        pull_load<Q, Real>(g, src, x, y, za, code_a, gen_a, ra);
-        if (two) pull_load<Q, Real>(g, src, x, y, za + 1, code_b, gen_b, rb);
-    }
+    pull_load<Q, Real>(g, src, x, y, za, code_a, edge_xy || plane_wraps(g, za), ra);
+    if (two) pull_load<Q, Real>(g, src, x, y, za + 1, code_b, edge_xy || plane_wraps(g, za + 1), rb);
     auto finish = [&](int z, int64_t cell, uint32_t code, const Real (&raw)[Q]) {
         Acc f[Q];
         const uint2 t = TYPED ? type_words(g, typemask, x, y, z, code) : make_uint2(0u, 0u);

@@ -252,6 +252,38 @@ class BoundaryHandling:
                          box.lo[2] + c // (box.nx * box.ny))
         return Masks(cm, frozen.typemask, frozen.counts, unflagged)
 
-    def apply(self, block, src, dst) -> None:
-        raise ValidationError("boundary links are fused into the stream-collide kernel on the "
-                              "B200 path; call stream_collide(..., handling=...)")
+    def apply(self, block, src, dst):
+        """Write the block's boundary links into dst from the post-collision
+        src (boundary.py:154-195): src / dst are ghost-inclusive (z, y, x, q)
+        host views.  The per-call host-view entry point of the kernel-slot
+        route (collide -> stream_pull -> apply); stream_collide fuses the
+        same rule into its sweep kernel.  Runs on the GPU
+        (lbm_slot_apply_links) with the frozen link lists."""
+        import torch
+        from .collision import SRT, kernel_params
+        st = self.stencil
+        if src.shape != dst.shape or src.ndim != 4 or src.shape[3] != st.q:
+            raise ValidationError(f"src / dst must be matching (z, y, x, {st.q}) views")
+        Z, Y, X, q = src.shape
+        kinds, dirs, cells = [], [], []
+        for kind, name in enumerate(_LINK_FLAGS):      # 0 NoSlip, 1 UBB, 2 Pressure
+            for i, zs, ys, xs in self.links[block.id][name]:
+                kinds.append(np.full(len(zs), kind, dtype=np.int32))
+                dirs.append(np.full(len(zs), i, dtype=np.int32))
+                cells.append((np.asarray(zs) * Y + np.asarray(ys)) * X + np.asarray(xs))
+        if not kinds:
+            return
+        kp = kernel_params(st, SRT(1.0), None, ubb_velocity=self.ubb_velocity,
+                           reference_density=self.reference_density)
+        for k in range(q):
+            kp.struct.pressure[k] = 2.0 * st.weights[k] * self.pressure_density
+        dev = torch.device("cuda", torch.cuda.current_device())
+        put = lambda a, dt: torch.from_numpy(np.ascontiguousarray(np.concatenate(a), dtype=dt)
+                                              ).to(dev)
+        t_kind, t_dir, t_cell = put(kinds, np.int32), put(dirs, np.int32), put(cells, np.int64)
+        t_src = torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64)).to(dev)
+        t_dst = torch.from_numpy(np.ascontiguousarray(dst, dtype=np.float64)).to(dev)
+        _lib.call("lbm_slot_apply_links", q, kp.ref, _lib.ptr(t_kind), _lib.ptr(t_dir),
+                  _lib.ptr(t_cell), int(t_cell.numel()), _lib.ptr(t_src), _lib.ptr(t_dst),
+                  _lib.stream_ptr(torch.cuda.current_stream(dev)))
+        dst[...] = t_dst.cpu().numpy()

@@ -259,6 +259,63 @@ def make_ownership():
     print("ownership:", len(parts), "partitions,", len(forests), "forests")
 
 
+APPLY_CASES = {  # name: (stencil, dims x, y, z)
+    "D3Q19": ("D3Q19", (7, 6, 5)),
+    "D3Q27": ("D3Q27", (6, 5, 6)),
+    "D2Q9": ("D2Q9", (9, 7, 1)),
+}
+
+
+def apply_flags(reg, dims, d):
+    """Interior flag codes of the apply goldens: a closed box - NoSlip walls,
+    a UBB lid (top y plane in 2D, top z plane in 3D), a Pressure outlet on
+    the high-x face - around Fluid with one NoSlip obstacle cell."""
+    nx, ny, nz = dims
+    f = np.full((nz, ny, nx), reg["NoSlip"], dtype=np.uint32)
+    if d == 3:
+        f[1:-1, 1:-1, 1:-1] = reg["Fluid"]
+        f[-1, 1:-1, 1:-1] = reg["UBB"]
+        f[1:-1, 1:-1, -1] = reg["Pressure"]
+    else:
+        f[:, 1:-1, 1:-1] = reg["Fluid"]
+        f[:, -1, 1:-1] = reg["UBB"]
+        f[:, 1:-1, -1] = reg["Pressure"]
+    f[nz // 2, ny // 2, nx // 2] = reg["NoSlip"]
+    return f
+
+
+def make_apply():
+    """BoundaryHandling.apply of the reference (lbm/boundary.py:154-195) on
+    random post-collision src / dst views of one block, every link type."""
+    import blocksim.lbm as L
+    from blocksim.blockforest import create_forest
+    rng = np.random.default_rng(55)
+    out = {}
+    for name, (sname, dims) in APPLY_CASES.items():
+        st = getattr(L, sname)
+        d = st.d
+
+        def prog(ctx):
+            forest = create_forest(ctx, (0, 0, 0, 1, 1, 1), (1, 1, 1), d=d,
+                                   periodic=(False, False, False), cells_per_block=dims)
+            handler = L.ensure_flags(forest)
+            blk = forest.local_blocks()[0]
+            blk.data["flags"].interior[...] = apply_flags(handler.registry, dims, d)
+            h = L.BoundaryHandling(forest, st, ubb_velocity=(0.03, -0.01, 0.02)[:3],
+                                   pressure_density=1.02, reference_density=0.99)
+            h.freeze()
+            shape = blk.data["flags"].view.shape + (st.q,)
+            src = st.weights * (1.0 + 0.1 * rng.uniform(-1, 1, shape))
+            dst = rng.standard_normal(shape)
+            res = dst.copy()
+            h.apply(blk, src, res)
+            return src, dst, res, {k: h.link_count(blk) for k in ("all",)}
+        src, dst, res, counts = SimRuntime(1, seed=0).run(prog)[0]
+        out[f"{name}__src"], out[f"{name}__dst"], out[f"{name}__out"] = src, dst, res
+        print("apply", name, counts)
+    np.savez(HERE / "apply.npz", **out)
+
+
 def make_units():
     """Reference unit functions on seeded random cells."""
     import blocksim.lbm as L
@@ -314,6 +371,8 @@ if __name__ == "__main__":
         make_slot()
     elif args == ["ownership"]:
         make_ownership()
+    elif args == ["apply"]:
+        make_apply()
     elif args == ["coupling"]:
         make_coupling()
     else:
@@ -323,3 +382,4 @@ if __name__ == "__main__":
             make_coupling()
             make_slot()
             make_ownership()
+            make_apply()

@@ -140,3 +140,67 @@ def test_slot_rejects_foreign_velocity_sets():
     raw, view = _view(name)
     with pytest.raises(P.ValidationError):
         kernel_slot.collide(view, GOLD[f"{name}__flags"], 1, int(GOLD[f"{name}__mode"]), p)
+
+
+# --------------------------------------------- BoundaryHandling.apply
+APPLY = np.load(Path(__file__).resolve().parent / "golden" / "apply.npz")
+APPLY_DIMS = {"D3Q19": (7, 6, 5), "D3Q27": (6, 5, 6), "D2Q9": (9, 7, 1)}
+
+
+def _apply_flags(reg, dims, d):
+    """tests/golden/make_golden.py:apply_flags, restated."""
+    nx, ny, nz = dims
+    f = np.full((nz, ny, nx), reg["NoSlip"], dtype=np.uint32)
+    inner = (slice(1, -1),) * 3 if d == 3 else (slice(None), slice(1, -1), slice(1, -1))
+    f[inner] = reg["Fluid"]
+    if d == 3:
+        f[-1, 1:-1, 1:-1] = reg["UBB"]
+        f[1:-1, 1:-1, -1] = reg["Pressure"]
+    else:
+        f[:, -1, 1:-1] = reg["UBB"]
+        f[:, 1:-1, -1] = reg["Pressure"]
+    f[nz // 2, ny // 2, nx // 2] = reg["NoSlip"]
+    return f
+
+
+@pytest.mark.parametrize("name", sorted(APPLY_DIMS))
+def test_oracle_apply_matches_reference(name):
+    """The C oracle's link rule (orc_apply_links) == the reference's apply."""
+    import ctypes
+    st = oracle.STENCILS[name]
+    dims = APPLY_DIMS[name]
+    d = 2 if name == "D2Q9" else 3
+    bits = {"Fluid": 1, "NoSlip": 2, "UBB": 4, "Pressure": 8, "Solid": 16}
+    nx, ny, nz = dims
+    Z, Y, X = nz + 2, ny + 2, nx + 2
+    flags = np.zeros((Z, Y, X), dtype=np.uint32)
+    flags[1:-1, 1:-1, 1:-1] = _apply_flags(bits, dims, d)
+    src = np.ascontiguousarray(np.moveaxis(APPLY[f"{name}__src"], 3, 0))
+    dst = np.ascontiguousarray(np.moveaxis(APPLY[f"{name}__dst"], 3, 0))
+    L = oracle.lbm_oracle._Links()
+    L.fluid, L.noslip, L.ubb, L.pressure = 1, 2, 4, 8
+    L.uwx, L.uwy, L.uwz, L.rho0, L.rho_w = 0.03, -0.01, 0.02, 0.99, 1.02
+    cst = oracle.lbm_oracle._cstencil(st)
+    oracle.lib().orc_apply_links(ctypes.byref(cst), oracle.lbm_oracle._ptr(src),
+                                 oracle.lbm_oracle._ptr(dst), oracle.lbm_oracle._ptr(flags),
+                                 X, Y, Z, ctypes.byref(L))
+    assert np.moveaxis(dst, 0, 3).tobytes() == APPLY[f"{name}__out"].tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(APPLY_DIMS))
+def test_boundary_handling_apply_bitwise_vs_reference(name):
+    import paper_1909_13772_b200 as P
+    st = getattr(P, name)
+    dims = APPLY_DIMS[name]
+    forest = P.create_forest(P.Context(), (0, 0, 0, 1, 1, 1), (1, 1, 1), d=st.d,
+                             periodic=(False, False, False), cells_per_block=dims)
+    reg = P.ensure_flags(forest).registry
+    blk = forest.local_blocks()[0]
+    blk.data["flags"].interior[...] = _apply_flags(reg, dims, st.d)
+    h = P.BoundaryHandling(forest, st, ubb_velocity=(0.03, -0.01, 0.02),
+                           pressure_density=1.02, reference_density=0.99)
+    h.freeze()
+    dst = APPLY[f"{name}__dst"].copy()
+    h.apply(blk, APPLY[f"{name}__src"], dst)
+    assert dst.tobytes() == APPLY[f"{name}__out"].tobytes()
