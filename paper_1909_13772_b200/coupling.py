@@ -376,25 +376,33 @@ def _released(old_in, new_in):
     return np.nonzero((old_in >= 0) & (new_in == -1))
 
 
-def _neighbour_mean_density(rho, donor, cells, stencil, rho0):
-    """Mean of rho over each cell's in-block donor neighbours, summed in
-    direction order; rho0 where a cell has none (system.py:60-77)."""
-    fz, fy, fx = cells
-    nz, ny, nx = rho.shape
-    acc = np.zeros(len(fz))
-    cnt = np.zeros(len(fz))
-    for cx, cy, cz in stencil.c[1:]:
-        tz, ty, tx = fz + cz, fy + cy, fx + cx
-        ok = (tz >= 0) & (tz < nz) & (ty >= 0) & (ty < ny) & (tx >= 0) & (tx < nx)
-        ok[ok] = donor[tz[ok], ty[ok], tx[ok]]
-        acc[ok] += rho[tz[ok], ty[ok], tx[ok]]
-        cnt[ok] += 1.0
-    return np.where(cnt > 0.0, acc / np.maximum(cnt, 1.0), float(rho0))
+def _cell_sums(vals, layout):
+    """sum over the q populations of each column of vals (q, n) in the
+    order numpy's `interior.sum(axis=-1)` uses on the host view of that
+    field layout (system.py:60): "fzyx" (q outermost) reduces element-wise
+    in direction order; "zyxf" (q contiguous) runs numpy's pairwise kernel,
+    eight partial sums combined as ((0+1)+(2+3))+((4+5)+(6+7)), then the
+    remaining directions in order.  Device tensors, fp64, every op rounded."""
+    q = vals.shape[0]
+    if layout == "fzyx" or q < 8:
+        acc = vals[0].clone()
+        for k in range(1, q):
+            acc = acc + vals[k]
+        return acc
+    part = [vals[j].clone() for j in range(8)]
+    top = q - q % 8
+    for i in range(8, top, 8):
+        for j in range(8):
+            part[j] = part[j] + vals[i + j]
+    acc = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]))
+    for k in range(top, q):
+        acc = acc + vals[k]
+    return acc
 
 
 def _surface_velocity(storage, block_id, uids, points):
     """v + w x (p - x) of each point's departing body, per component in the
-    reference's operation order."""
+    reference's operation order (host, a few values per released cell)."""
     u = np.empty((len(uids), 3))
     for uid in np.unique(uids):
         body = storage.bodies.get(int(uid))
@@ -414,31 +422,67 @@ def reinitialize_uncovered(pdf, old_mapping, new_mapping, *, handling=None, bodi
                            reference_density=1.0):
     """Cells a body released get the equilibrium of the mean density of
     their surviving in-block fluid neighbours and the departing body's
-    surface velocity at the cell centre (system.py:26-100).  Host edit of the
-    src slot (re-uploaded before the next sweep); returns the local count."""
-    from .lbm.collision import equilibrium
-    forest, st = pdf.forest, pdf.stencil
-    count = 0
-    for block in forest.local_blocks():
+    surface velocity at the cell centre (system.py:26-100).  Returns the
+    local count.
+
+    On the device: R_n is materialised once as a dense tensor, the donor
+    densities are summed in numpy's order for the field's layout
+    (_cell_sums), averaged in direction order, the equilibrium of the
+    released cells is computed by the equilibrium kernel and written into
+    R_n, which becomes the device state (the next sweep collides it).  No
+    field crosses PCIe; the host only decides which cells are involved."""
+    import torch
+    from .lbm.collision import _device
+    forest, st, lat = pdf.forest, pdf.stencil, pdf.lattice
+    plan = []      # (box offset, block, cells, donor, uids) of blocks with released cells
+    for block, off in zip(lat.box.blocks, lat.box.offsets):
         new_ow, old_ow = new_mapping.owner[block.id], old_mapping.owner.get(block.id)
         if old_ow is None or old_ow.shape != new_ow.shape:
             raise ValidationError(f"mappings disagree on {block.id}")
         old_in, new_in = old_ow[1:-1, 1:-1, 1:-1], new_ow[1:-1, 1:-1, 1:-1]
         cells = _released(old_in, new_in)
-        if len(cells[0]) == 0:
-            continue
-        count += len(cells[0])
-        interior = pdf.src(block).interior
-        donor = (old_in == -1) & (new_in == -1)
-        if handling is not None:
-            flags = block.data[handling.flags_key].field.view_nosync[1:-1, 1:-1, 1:-1, 0]
-            donor &= (flags & handling.fluid_mask(block)) != 0
-        rho_bar = _neighbour_mean_density(interior.sum(axis=-1), donor, cells, st,
-                                          reference_density)
+        if len(cells[0]):
+            donor = (old_in == -1) & (new_in == -1)
+            if handling is not None:
+                flags = block.data[handling.flags_key].field.view_nosync[1:-1, 1:-1, 1:-1, 0]
+                donor &= (flags & handling.fluid_mask(block)) != 0
+            plan.append((off, block, cells, donor, old_in[cells]))
+    if not plan:
+        return 0
+    if lat.host_changed():
+        lat.upload_host()
+    full = lat.rform_device()
+    dev = _device()
+    count = 0
+    for (ox, oy, oz), block, (fz, fy, fx), donor, uids in plan:
+        n = len(fz)
+        count += n
+        nz, ny, nx = donor.shape
+        acc = torch.zeros(n, dtype=torch.float64, device=dev)
+        cnt = np.zeros(n)
+        for cx, cy, cz in st.c[1:]:
+            tz, ty, tx = fz + cz, fy + cy, fx + cx
+            ok = (tz >= 0) & (tz < nz) & (ty >= 0) & (ty < ny) & (tx >= 0) & (tx < nx)
+            ok[ok] = donor[tz[ok], ty[ok], tx[ok]]
+            if ok.any():
+                idx = torch.from_numpy(np.flatnonzero(ok)).to(dev)
+                zz, yy, xx = (torch.from_numpy(v[ok] + o + 1).to(dev)
+                              for v, o in ((tz, oz), (ty, oy), (tx, ox)))
+                acc[idx] = acc[idx] + _cell_sums(full[:, zz, yy, xx], pdf.layout)
+                cnt[ok] += 1.0
+        cnt_t = torch.from_numpy(cnt).to(dev)
+        rho_bar = torch.where(cnt_t > 0.0, acc / torch.clamp(cnt_t, min=1.0),
+                              torch.full_like(acc, float(reference_density)))
         c0, _ = forest.cell_centers(block.id)
-        points = [c0[a] + cells[2 - a].astype(np.float64) for a in range(3)]
-        u = _surface_velocity(block.data[bodies_key], block.id, old_in[cells], points)
-        interior[cells] = equilibrium(rho_bar, u, st)
+        points = [c0[a] + (fx, fy, fz)[a].astype(np.float64) for a in range(3)]
+        u = torch.from_numpy(_surface_velocity(block.data[bodies_key], block.id, uids,
+                                               points)).to(dev)
+        feq = torch.empty((n, st.q), dtype=torch.float64, device=dev)
+        _lib.call("lbm_equilibrium_cells", st.q, _lib.ptr(rho_bar), _lib.ptr(u), _lib.ptr(feq), n,
+                  _lib.stream_ptr(torch.cuda.current_stream(dev)))
+        zz, yy, xx = (torch.from_numpy(v + o + 1).to(dev) for v, o in ((fz, oz), (fy, oy), (fx, ox)))
+        full[:, zz, yy, xx] = feq.T
+    lat.adopt_rform(full)
     return count
 
 

@@ -296,6 +296,28 @@ class DeviceLattice:
         kind, t = self.readout_device()
         return kind, t.cpu().numpy()
 
+    def rform_device(self):
+        """R_n as a dense ghost-inclusive (q, Z, Y, X) fp64 device tensor:
+        S(G_{n-1}) on the interior, the stored ghost shell around it."""
+        kind, inner = self.readout_device()
+        if kind == "full":
+            return inner
+        b = self.box
+        full = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
+                           device=self.device)
+        _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(self.buf[self.cur]), _lib.ptr(full),
+                  self._sp())
+        full[:, 1:-1, 1:-1, 1:-1] = inner
+        return full
+
+    def adopt_rform(self, full):
+        """Make a (possibly edited) dense R_n the device state (kind R): the
+        next sweep collides it again, exactly as after a host upload."""
+        _lib.call("lbm_pack_rform", self.gref, _lib.ptr(full), _lib.ptr(self.buf[self.cur]),
+                  self._sp())
+        self.cur_kind, self.prev_kind, self.coll_key = "R", None, None
+        self.host_state, self.snapshot, self._dst_synced = "device", None, None
+
     def _wrap_ghosts(self, full):
         """Covered ghost cells of a ghost-inclusive (q, Z, Y, X) box = their
         periodic images inside the box (x, then y rows incl. x ghosts, then
@@ -401,15 +423,8 @@ class DeviceLattice:
             # model / flags changed between sweeps: the stored G_n was collided
             # with the old key.  Rebuild R_n = S(G_{n-1}) (old pull masks) into
             # buffer[cur] - its ghost shell stays valid - and collide again.
-            kind, inner = self.readout_device()
-            b = self.box
-            full = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
-                               device=self.device)
-            _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(self.buf[self.cur]),
-                      _lib.ptr(full), self._sp())
-            full[:, 1:-1, 1:-1, 1:-1] = inner
-            _lib.call("lbm_pack_rform", self.gref, _lib.ptr(full), _lib.ptr(self.buf[self.cur]),
-                      self._sp())
+            _lib.call("lbm_pack_rform", self.gref, _lib.ptr(self.rform_device()),
+                      _lib.ptr(self.buf[self.cur]), self._sp())
             self.cur_kind = "R"
         if self.cur_kind != "R":
             raise ValidationError("PDF field has no device state")

@@ -96,6 +96,7 @@ class PdfField:
         self.key = key
         self.dst_key = key + ".dst"
         self.dtype = dtype
+        self.layout = layout
         self._lattice = None
         self._mirror = _Mirror(self)
         self._dst_mirror = _DstMirror(self)

@@ -535,6 +535,14 @@ COUPLING_CASES = {
                               bodies=[((8.2, 8.1, 7.9), 3.0, 1.0, (0.0, 0.0, 0.0),
                                        (0.0, 0.0, 0.0))],
                               steps=12, move=False, layout="zyxf"),
+    # the AoS layout ("zyxf": the reference sums densities with numpy's
+    # pairwise kernel there) with D3Q27 and moving bodies, 2 blocks in z:
+    # released cells are re-initialised on the device in that order
+    "moving_d3q27_aos": dict(stencil="D3Q27", dims=(14, 12, 16), root_dims=(1, 1, 2),
+                             model=("SRT", 1.5), force=None,
+                             bodies=[((6.6, 5.9, 7.3), 2.8, 60.0, (0.11, 0.07, -0.09),
+                                      (0.004, -0.002, 0.003))],
+                             steps=7, move=True, layout="zyxf"),
 }
 
 
