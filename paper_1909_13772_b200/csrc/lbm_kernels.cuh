@@ -33,7 +33,8 @@ struct KGrid {
     int64_t plane;                 // (ny+2) * pitch
     int64_t zstride;               // q * plane
     int plane32, zstride32;        // the same as int (check_grid range-checks every delta)
-    int link_hint;                 // 1: z-planes large against L2 (see ldg_keep)
+    int link_hint;                 // bit 0: z-planes large against L2 (see ldg_keep);
+                                   // bits 1..: cell-mask rows prefetched ahead (prefetch_mask)
     // own-relative element deltas, indexed by reference direction i (host-computed):
     int dpull[27];   // source of the pull of direction i: slot(i) plane - c_i . (1, pitch, zstride)
     int dlink[27];   // bounce-back source: own cell, slot(opp(i)) plane
@@ -102,6 +103,19 @@ __device__ __forceinline__ T ldg_keep(const T* p) {
         asm volatile("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
                      "ld.global.nc.L2::cache_hint.f32 %0, [%1], pol;\n}" : "=f"(v) : "l"(p));
         return (T)v;
+    }
+}
+
+// L2 prefetch of the cell-mask words `rows` rows ahead of this cell (same
+// x, plane order): the block that reads them is launched about one resident
+// window later, so its mask load - which every pull address waits on - hits
+// L2 instead of paying a DRAM round trip.
+__device__ __forceinline__ void prefetch_mask(const KGrid& g, const uint32_t* cellmask, int64_t cell,
+                                              int64_t ncells) {
+    const int ahead = g.link_hint >> 1;
+    if (ahead > 0 && cellmask) {
+        const int64_t c = cell + (int64_t)ahead * g.nx;
+        if (c < ncells) asm volatile("prefetch.global.L2 [%0];" ::"l"(cellmask + c));
     }
 }
 
@@ -335,7 +349,7 @@ __device__ __forceinline__ void pull_load(const KGrid& g, const Real* __restrict
             // later); that read keeps the line in L2 (evict_last) for the
             // second one instead of leaving it to a whole plane of traffic.
             if constexpr (link_hint<Real>() && D::cz[i] == -1) {
-                if (g.link_hint && ((((code >> i) & 1u) != 0u) || !(code & LBM_MASK_FLUID)))
+                if ((g.link_hint & 1) && ((((code >> i) & 1u) != 0u) || !(code & LBM_MASK_FLUID)))
                     raw[i] = ldg_keep(sp + d);
                 else
                     raw[i] = __ldg(sp + d);
@@ -509,6 +523,9 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FO
     // cellmask == NULL: every cell fluid, no links (periodic runs without a
     // boundary handling) - saves the 4 B/cell mask read
     const uint32_t code = cellmask ? __ldg(cellmask + cell) : LBM_MASK_FLUID;
+    // D3Q19 only: the D3Q27 MRT kernels (config 2) lose 9 % to the extra
+    // registers even with the prefetch switched off (measured)
+    if constexpr (Q == 19) prefetch_mask(g, cellmask, cell, (int64_t)g.nx * g.ny * g.nz);
     using Acc = AccOf<Real>;
     Acc f[Q];
     pull_cell<Q, Real, Acc, MOVING ? 2 : 0>(g, p, src, x, y, z, code, typemask, generic, f);
@@ -580,6 +597,13 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FO
     const uint32_t code_a = cellmask ? __ldg(cellmask + cell_a) : LBM_MASK_FLUID;
     const uint32_t code_b = !two ? 0u : cellmask ? __ldg(cellmask + cell_a + plane_cells)
                                                  : LBM_MASK_FLUID;
+    {   // both planes of the pair, (link_hint >> 1) pair-rows ahead; a row
+        // index beyond ny continues in the next plane pair
+        const int64_t ncells = (int64_t)g.nx * g.ny * g.nz;
+        const int64_t c = (g.link_hint >> 1) > g.ny - 1 - y ? cell_a + plane_cells : cell_a;
+        prefetch_mask(g, cellmask, c, ncells);
+        prefetch_mask(g, cellmask, c + plane_cells, ncells);
+    }
     using Acc = AccOf<Real>;
     Real ra[Q], rb[Q];
     pull_load<Q, Real>(g, src, x, y, za, code_a, edge_xy || plane_wraps(g, za), ra);

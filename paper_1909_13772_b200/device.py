@@ -22,6 +22,7 @@ user), readout (host arrays touched) and mask builds; never inside the step.
 from __future__ import annotations
 
 import ctypes
+import gc
 
 import numpy as np
 import torch
@@ -32,6 +33,20 @@ from .errors import BackendError, ValidationError
 
 def _round_up(v, m):
     return (v + m - 1) // m * m
+
+
+def hbm_empty(n, dtype, device) -> torch.Tensor:
+    """A large HBM buffer.  Lattices of dropped PdfFields sit in reference
+    cycles (forest -> slot handler -> PdfField -> lattice -> forest, as in
+    the reference's object graph) that only the cyclic GC frees, and the GC
+    is not driven by device memory: on an allocation failure collect them
+    and retry once before reporting out of memory."""
+    try:
+        return torch.empty(n, dtype=dtype, device=device)
+    except torch.OutOfMemoryError:
+        gc.collect()
+        torch.cuda.empty_cache()
+        return torch.empty(n, dtype=dtype, device=device)
 
 
 class RankBox:
@@ -178,8 +193,8 @@ class DeviceLattice:
         self.elems = int(_lib.load().lbm_field_elems(self.gref))
         if self.elems <= 0:
             _lib.call("lbm_field_elems", self.gref)
-        self.buf = [torch.empty(self.elems, dtype=self.tdtype, device=self.device),
-                    torch.empty(self.elems, dtype=self.tdtype, device=self.device)]
+        self.buf = [hbm_empty(self.elems, self.tdtype, self.device),
+                    hbm_empty(self.elems, self.tdtype, self.device)]
         self.cur = 0
         self.cur_kind = None      # None / "R" / "G"
         self.prev_kind = None     # None / "R" / "G"
@@ -279,14 +294,13 @@ class DeviceLattice:
         b = self.box
         if self.cur_kind == "R" or self.prev_kind == "R":
             src = self.buf[self.cur] if self.cur_kind == "R" else self.buf[1 - self.cur]
-            out = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
-                              device=self.device)
+            out = hbm_empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), torch.float64, self.device)
             _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(src), _lib.ptr(out), self._sp())
             return "full", out
         if self.cur_kind is None:
             raise ValidationError("PDF field has no device state")
         m = self.stream_masks
-        out = torch.empty((self.q, b.nz, b.ny, b.nx), dtype=torch.float64, device=self.device)
+        out = hbm_empty((self.q, b.nz, b.ny, b.nx), torch.float64, self.device)
         _lib.call("lbm_stream_only", self.gref, self._kp_stream.ref,
                   _lib.ptr(self.buf[1 - self.cur]), _lib.ptr(m.cellmask), _lib.ptr(m.typemask),
                   _lib.ptr(out), self._sp())
@@ -303,8 +317,7 @@ class DeviceLattice:
         if kind == "full":
             return inner
         b = self.box
-        full = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
-                           device=self.device)
+        full = hbm_empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), torch.float64, self.device)
         _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(self.buf[self.cur]), _lib.ptr(full),
                   self._sp())
         full[:, 1:-1, 1:-1, 1:-1] = inner
@@ -345,8 +358,7 @@ class DeviceLattice:
         every sweep overwrites them before use, so they carry no state.)"""
         self.join_streams()
         b = self.box
-        full = torch.empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), dtype=torch.float64,
-                           device=self.device)
+        full = hbm_empty((self.q, b.nz + 2, b.ny + 2, b.nx + 2), torch.float64, self.device)
         if which == "dst":
             src = self.buf[1 - self.cur] if self.prev_kind == "G" else self.buf[self.cur]
             _lib.call("lbm_unpack_rform", self.gref, _lib.ptr(src), _lib.ptr(full), self._sp())

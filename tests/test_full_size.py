@@ -20,6 +20,7 @@ goldens) runs the same inputs on the host cores.  Reference path matched:
 Host RAM: the 512^3 oracle holds two 20.6 GB fields (the GPU box has
 ~196 GB); comparisons stream the GPU's readout in z-chunks.
 """
+import gc
 import os
 import time
 
@@ -54,6 +55,8 @@ def _gpu_run(config, dtype, steps):
     assert kind == "interior"
     torch.cuda.synchronize()
     del forest, pdf, handling
+    gc.collect()          # the forest / field / lattice cycle holds the HBM buffers
+    torch.cuda.empty_cache()
     return out, dims
 
 
@@ -146,6 +149,7 @@ def test_512cubed_fp64_bitwise_vs_oracle(config):
     print(f"{config} 512^3 x {steps}: gpu {t1 - t0:.1f} s, oracle {t2 - t1:.1f} s, "
           f"bitwise={equal} max|d|={worst:.3e}")
     del dom, out
+    gc.collect()
     torch.cuda.empty_cache()
     assert equal, f"{config}: GPU != oracle, max|d| = {worst:.3e} (tol 1e-12)"
 
@@ -167,6 +171,7 @@ def test_config4_fp32_512cubed_200_steps_within_1e5():
     rel = _rel_err(got, ref)
     print(f"config 4 fp32 512^3 x 200: max rel err vs fp64 = {rel:.3e}")
     del ref, got
+    gc.collect()
     torch.cuda.empty_cache()
     assert rel < TOL_F32_REL, rel
 
@@ -181,6 +186,7 @@ def test_config2_fp32_256cubed_500_steps_within_1e5():
     rel = _rel_err(got, ref)
     print(f"config 2 fp32 256^3 x 500: max rel err vs fp64 = {rel:.3e}")
     del ref, got
+    gc.collect()
     torch.cuda.empty_cache()
     assert rel < TOL_F32_REL, rel
 
