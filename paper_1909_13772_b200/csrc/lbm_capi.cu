@@ -92,11 +92,14 @@ int check_grid(const lbm_grid_t* g, KGrid* k) {
     // cell-mask rows prefetched into L2 ahead of the sweep (prefetch_mask).
     // Measured on B200, config 4 (rows ahead -> fraction of the HBM roofline):
     // fp32 0: 0.861, 32: 0.897, 64: 0.904, 128: 0.905, 300: 0.895, 600: 0.867;
-    // fp64 0: 0.942, 32: 0.946, 64: 0.947, 128: 0.944, 600: 0.925.
+    // fp64 0: 0.942, 32: 0.946, 64: 0.947, 128: 0.944, 600: 0.925;
+    // config 2 (D3Q27 fp32, 256^2 planes) 0: 0.923, 4: 0.935, 16: 0.941,
+    // 32: 0.946, 64: 0.936, 128: 0.935.
     // LBM_B200_MASK_AHEAD=n overrides (0: off).
     // (Packed into KGrid::link_hint bits 1.. so the kernel argument layout -
-    // and with it the register allocation of the D3Q27 kernels - is unchanged.)
-    int ahead = g->real_bytes == 4 ? 128 : 64;
+    // and with it the register allocation of the D3Q27 kernels - is unchanged:
+    // a separate field cost config 2 9 % through a changed spill placement.)
+    int ahead = g->real_bytes == 8 ? 64 : (g->q == 27 ? 32 : 128);
     if (const char* h = getenv("LBM_B200_MASK_AHEAD")) ahead = atoi(h) > 0 ? atoi(h) : 0;
     if (ahead > (1 << 20)) ahead = 1 << 20;
     k->link_hint |= ahead << 1;

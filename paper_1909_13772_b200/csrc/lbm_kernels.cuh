@@ -523,9 +523,7 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FO
     // cellmask == NULL: every cell fluid, no links (periodic runs without a
     // boundary handling) - saves the 4 B/cell mask read
     const uint32_t code = cellmask ? __ldg(cellmask + cell) : LBM_MASK_FLUID;
-    // D3Q19 only: the D3Q27 MRT kernels (config 2) lose 9 % to the extra
-    // registers even with the prefetch switched off (measured)
-    if constexpr (Q == 19) prefetch_mask(g, cellmask, cell, (int64_t)g.nx * g.ny * g.nz);
+    prefetch_mask(g, cellmask, cell, (int64_t)g.nx * g.ny * g.nz);
     using Acc = AccOf<Real>;
     Acc f[Q];
     pull_cell<Q, Real, Acc, MOVING ? 2 : 0>(g, p, src, x, y, z, code, typemask, generic, f);
