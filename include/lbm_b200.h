@@ -51,6 +51,11 @@
  *                       per-call "b200" backend of blocksim._kernels.
  *   lbm_bind_params     re-binds a parameter block's device-side state (MRT
  *                       constant tables) before a captured CUDA graph replays.
+ *   lbm_fill_equilibrium_planes / lbm_collide_only_planes / lbm_moments_planes
+ *                       the same three steps on a range of z-planes, for a
+ *                       pipelined job (fill_equilibrium -> K x stream_collide
+ *                       -> macroscopic, sweep.py:51-183) whose host<->device
+ *                       copies overlap the sweeps plane chunk by plane chunk.
  *   lbm_face_span       geometry of the per-step z-face ghost exchange
  *                       (field/ghost.py:112-173,202-264), restricted to the
  *                       PDF directions that cross the face.
@@ -79,7 +84,7 @@
 extern "C" {
 #endif
 
-#define LBM_B200_ABI_VERSION 5
+#define LBM_B200_ABI_VERSION 6
 
 /* status codes */
 #define LBM_OK 0
@@ -284,6 +289,30 @@ int lbm_unpack_rform(const lbm_grid_t* g, const void* pdf, double* dense,
  * layout (R-form) - equilibrium() op order (collision.py:150-154). */
 int lbm_fill_equilibrium(const lbm_grid_t* g, const double* rho,
                          const double* u, void* pdf, void* stream);
+
+/* Plane-range forms (ABI 6) for pipelined jobs: the same arithmetic as the
+ * whole-box calls above, restricted to interior planes [z0, z1).
+ *   fill_planes: rho (nz,ny,nx) / u (nz,ny,nx,3) are DENSE interior arrays of
+ *     the whole box (device); ghost cells take the nearest interior cell's
+ *     values (each coordinate clamped: the shell fill_equilibrium_arrays
+ *     builds).  Writes the ghost-inclusive planes of [z0, z1), plus the z
+ *     ghost plane at either end of the box when z0 == 0 / z1 == nz; when
+ *     pdf_shell != NULL the ghost cells of those planes go there too (the
+ *     second field's shell, as lbm_copy_shell would give it).
+ *   collide_only_planes: lbm_collide_only on planes [z0, z1).
+ *   moments_planes: lbm_moments on planes [z0, z1); rho / u are whole-box
+ *     arrays, only those planes are written. */
+int lbm_fill_equilibrium_planes(const lbm_grid_t* g, const double* rho,
+                                const double* u, int z0, int z1, void* pdf,
+                                void* pdf_shell, void* stream);
+int lbm_collide_only_planes(const lbm_grid_t* g, const lbm_params_t* p,
+                            void* pdf, const uint32_t* cellmask, int z0,
+                            int z1, void* stream);
+int lbm_moments_planes(const lbm_grid_t* g, const lbm_params_t* p,
+                       const void* src, const uint32_t* cellmask,
+                       const uint32_t* typemask, int stream_form, int z0,
+                       int z1, double* rho, double* u, int* bad_count,
+                       void* stream);
 
 /* Flag validation + link masks from ghost-inclusive flags (Z, Y, X) uint32.
  * bits: [0]=Fluid [1]=NoSlip [2]=UBB [3]=Pressure [4]=Solid registry masks.

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
 
 LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
 ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
-ABI_VERSION = 5
+ABI_VERSION = 6
 SRT, TRT, MRT, SRT_FIELD = 0, 1, 2, 3
 MASK_FLUID = 0x1
 MASK_UBB = 0x80000000
@@ -33,6 +33,7 @@ EXPORTS = (
     "lbm_ipc_export", "lbm_ipc_open", "lbm_ipc_close",
     "lbm_bind_params", "lbm_slot_collide", "lbm_slot_stream_pull", "lbm_refresh_fluid_mask",
     "lbm_map_spheres", "lbm_copy_shell", "lbm_slot_apply_links",
+    "lbm_fill_equilibrium_planes", "lbm_collide_only_planes", "lbm_moments_planes",
 )
 
 
@@ -117,6 +118,9 @@ def load(path: Path | None = None):
         "lbm_map_spheres": ([I, P, P, P, P, P, P, ctypes.c_uint32, P, P], I),
         "lbm_copy_shell": ([G, P, P, P], I),
         "lbm_slot_apply_links": ([I, PR, P, P, P, I64, P, P, P], I),
+        "lbm_fill_equilibrium_planes": ([G, P, P, I, I, P, P, P], I),
+        "lbm_collide_only_planes": ([G, PR, P, P, I, I, P], I),
+        "lbm_moments_planes": ([G, PR, P, P, P, I, I, I, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -805,8 +805,9 @@ int lbm_stream_wait(const void* flag, uint32_t value, void* stream) {
     return LBM_OK;
 }
 
-int lbm_collide_only(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,
-                     const uint32_t* cellmask, void* stream) {
+static int collide_only_range(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,
+                              const uint32_t* cellmask, int z0, int z1, void* stream,
+                              const char* who) {
     KGrid k;
     KParams kp;
     cudaStream_t s = (cudaStream_t)stream;
@@ -814,12 +815,23 @@ int lbm_collide_only(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,
     if (st != LBM_OK) return st;
     if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
     if (!pdf || !cellmask) return fail(LBM_EINVAL, "NULL buffer");
+    if (z0 < 0 || z1 > g->nz || z0 > z1) return fail(LBM_EINVAL, "bad plane range [%d, %d)", z0, z1);
     cudaError_t e = g->real_bytes == 8
                         ? unit_f64::collide_only(g->q, p->model, p->force_mode, k, kp, pdf,
-                                                 cellmask, s)
+                                                 cellmask, z0, z1, s)
                         : unit_f32::collide_only(g->q, p->model, p->force_mode, k, kp, pdf,
-                                                 cellmask, s);
-    return cuda_status(e, "lbm_collide_only");
+                                                 cellmask, z0, z1, s);
+    return cuda_status(e, who);
+}
+
+int lbm_collide_only(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,
+                     const uint32_t* cellmask, void* stream) {
+    return collide_only_range(g, p, pdf, cellmask, 0, g ? g->nz : 0, stream, "lbm_collide_only");
+}
+
+int lbm_collide_only_planes(const lbm_grid_t* g, const lbm_params_t* p, void* pdf,
+                            const uint32_t* cellmask, int z0, int z1, void* stream) {
+    return collide_only_range(g, p, pdf, cellmask, z0, z1, stream, "lbm_collide_only_planes");
 }
 
 int lbm_stream_only(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
@@ -838,9 +850,10 @@ int lbm_stream_only(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
     return cuda_status(e, "lbm_stream_only");
 }
 
-int lbm_moments(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
-                const uint32_t* cellmask, const uint32_t* typemask, int stream_form, double* rho,
-                double* u, int* bad_count, void* stream) {
+static int moments_range(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
+                         const uint32_t* cellmask, const uint32_t* typemask, int stream_form,
+                         int z0, int z1, double* rho, double* u, int* bad_count, void* stream,
+                         const char* who) {
     KGrid k;
     KParams kp;
     cudaStream_t s = (cudaStream_t)stream;
@@ -849,12 +862,27 @@ int lbm_moments(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
     if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
     if (!src || !rho || !u || !bad_count) return fail(LBM_EINVAL, "NULL buffer");
     if (stream_form && (!cellmask || !typemask)) return fail(LBM_EINVAL, "NULL mask");
+    if (z0 < 0 || z1 > g->nz || z0 > z1) return fail(LBM_EINVAL, "bad plane range [%d, %d)", z0, z1);
     const int guo = p->force_mode == LBM_FORCE_GUO || p->force_mode == LBM_FORCE_GUO_X;
     cudaError_t e = g->real_bytes == 8 ? unit_f64::moments(g->q, guo, k, kp, src, cellmask, typemask,
-                                                           stream_form, rho, u, bad_count, s)
+                                                           stream_form, rho, u, bad_count, z0, z1, s)
                                        : unit_f32::moments(g->q, guo, k, kp, src, cellmask, typemask,
-                                                           stream_form, rho, u, bad_count, s);
-    return cuda_status(e, "lbm_moments");
+                                                           stream_form, rho, u, bad_count, z0, z1, s);
+    return cuda_status(e, who);
+}
+
+int lbm_moments(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
+                const uint32_t* cellmask, const uint32_t* typemask, int stream_form, double* rho,
+                double* u, int* bad_count, void* stream) {
+    return moments_range(g, p, src, cellmask, typemask, stream_form, 0, g ? g->nz : 0, rho, u,
+                         bad_count, stream, "lbm_moments");
+}
+
+int lbm_moments_planes(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
+                       const uint32_t* cellmask, const uint32_t* typemask, int stream_form, int z0,
+                       int z1, double* rho, double* u, int* bad_count, void* stream) {
+    return moments_range(g, p, src, cellmask, typemask, stream_form, z0, z1, rho, u, bad_count,
+                         stream, "lbm_moments_planes");
 }
 
 int lbm_pack_rform(const lbm_grid_t* g, const double* dense, void* pdf, void* stream) {
@@ -889,6 +917,26 @@ int lbm_fill_equilibrium(const lbm_grid_t* g, const double* rho, const double* u
     cudaError_t e = g->real_bytes == 8 ? unit_f64::fill_eq(g->q, k, rho, u, pdf, s)
                                        : unit_f32::fill_eq(g->q, k, rho, u, pdf, s);
     return cuda_status(e, "lbm_fill_equilibrium");
+}
+
+int lbm_fill_equilibrium_planes(const lbm_grid_t* g, const double* rho, const double* u, int z0,
+                                int z1, void* pdf, void* pdf_shell, void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!rho || !u || !pdf) return fail(LBM_EINVAL, "NULL buffer");
+    if (pdf == pdf_shell) return fail(LBM_EINVAL, "pdf_shell must be the other field");
+    if (z0 < 0 || z1 > g->nz || z0 > z1) return fail(LBM_EINVAL, "bad plane range [%d, %d)", z0, z1);
+    // ghost-inclusive planes: interior z0..z1-1 are zg = z0+1 .. z1, plus the
+    // z ghost planes at either end of the box
+    const int zg0 = z0 == 0 ? 0 : z0 + 1;
+    const int zg1 = z1 == g->nz ? g->nz + 2 : z1 + 1;
+    if (z0 == z1) return LBM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = g->real_bytes == 8
+                        ? unit_f64::fill_eq_dense(g->q, k, rho, u, zg0, zg1, pdf, pdf_shell, s)
+                        : unit_f32::fill_eq_dense(g->q, k, rho, u, zg0, zg1, pdf, pdf_shell, s);
+    return cuda_status(e, "lbm_fill_equilibrium_planes");
 }
 
 int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags, const uint32_t bits[5],

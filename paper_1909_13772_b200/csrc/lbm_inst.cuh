@@ -228,11 +228,12 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
 }
 
 template <int Q, int MODEL, int FORCE>
-cudaError_t collide_t(const KGrid& g, const KParams& p, void* pdf, const uint32_t* cm,
-                      cudaStream_t s) {
+cudaError_t collide_t(const KGrid& g, const KParams& p, void* pdf, const uint32_t* cm, int z0,
+                      int z1, cudaStream_t s) {
+    if (z1 <= z0) return cudaSuccess;
     dim3 b = cell_block(g.nx);
-    dim3 grid((g.nx + b.x - 1) / b.x, g.ny, g.nz);
-    k_collide_only<Q, LBM_REAL, MODEL, FORCE><<<grid, b, 0, s>>>(g, p, (LBM_REAL*)pdf, cm);
+    dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
+    k_collide_only<Q, LBM_REAL, MODEL, FORCE><<<grid, b, 0, s>>>(g, p, (LBM_REAL*)pdf, cm, z0);
     return cudaGetLastError();
 }
 
@@ -289,13 +290,13 @@ cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p,
 }
 
 cudaError_t collide_only(int q, int model, int force, const KGrid& g, const KParams& p, void* pdf,
-                         const uint32_t* cm, cudaStream_t s) {
+                         const uint32_t* cm, int z0, int z1, cudaStream_t s) {
     if (model == LBM_SRT_FIELD) model = 4;
     else if (model == LBM_MRT && p.mrt_fast) model = 3;
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         return by_model<Q>(model, force, [&](auto Mc, auto Fc) {
-            return collide_t<Q, decltype(Mc)::value, decltype(Fc)::value>(g, p, pdf, cm, s);
+            return collide_t<Q, decltype(Mc)::value, decltype(Fc)::value>(g, p, pdf, cm, z0, z1, s);
         });
     });
 }
@@ -313,17 +314,18 @@ cudaError_t stream_only(int q, const KGrid& g, const KParams& p, const void* src
 
 cudaError_t moments(int q, int guo, const KGrid& g, const KParams& p, const void* src,
                     const uint32_t* cm, const uint32_t* tmk, int stream_form, double* rho,
-                    double* u, int* bad, cudaStream_t s) {
+                    double* u, int* bad, int z0, int z1, cudaStream_t s) {
+    if (z1 <= z0) return cudaSuccess;
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         dim3 b = cell_block(g.nx);
-        dim3 grid((g.nx + b.x - 1) / b.x, g.ny, g.nz);
+        dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
         if (guo)
             k_moments<Q, LBM_REAL, 1><<<grid, b, 0, s>>>(g, p, (const LBM_REAL*)src, cm, tmk,
-                                                         stream_form, rho, u, bad);
+                                                         stream_form, rho, u, bad, z0);
         else
             k_moments<Q, LBM_REAL, 0><<<grid, b, 0, s>>>(g, p, (const LBM_REAL*)src, cm, tmk,
-                                                         stream_form, rho, u, bad);
+                                                         stream_form, rho, u, bad, z0);
         return cudaGetLastError();
     });
 }
@@ -349,6 +351,19 @@ cudaError_t fill_eq(int q, const KGrid& g, const double* rho, const double* u, v
         dim3 b = cell_block(g.nx + 2);
         dim3 grid((g.nx + 2 + b.x - 1) / b.x, g.ny + 2, g.nz + 2);
         k_fill_eq<Q, LBM_REAL><<<grid, b, 0, s>>>(g, rho, u, (LBM_REAL*)pdf);
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t fill_eq_dense(int q, const KGrid& g, const double* rho, const double* u, int zg0,
+                          int zg1, void* pdf, void* shell, cudaStream_t s) {
+    if (zg1 <= zg0) return cudaSuccess;
+    return by_q(q, [&](auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        dim3 b = cell_block(g.nx + 2);
+        dim3 grid((g.nx + 2 + b.x - 1) / b.x, g.ny + 2, zg1 - zg0);
+        k_fill_eq_dense<Q, LBM_REAL><<<grid, b, 0, s>>>(g, rho, u, zg0, (LBM_REAL*)pdf,
+                                                        (LBM_REAL*)shell);
         return cudaGetLastError();
     });
 }

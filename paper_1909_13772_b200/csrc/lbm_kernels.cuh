@@ -625,10 +625,10 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FO
 // G_0 = C(R_0): collide fluid interior cells in place.
 template <int Q, typename Real, int MODEL, int FORCE>
 __global__ void __launch_bounds__(128) k_collide_only(KGrid g, KParams p, Real* __restrict__ pdf,
-                                                      const uint32_t* __restrict__ cellmask) {
+                                                      const uint32_t* __restrict__ cellmask, int z0) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y;
-    const int z = blockIdx.z;
+    const int z = z0 + blockIdx.z;
     if (x >= g.nx) return;
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
     const uint32_t code = cellmask[cell];
@@ -675,11 +675,11 @@ __global__ void __launch_bounds__(128) k_moments(KGrid g, KParams p, const Real*
                                                  const uint32_t* __restrict__ cellmask,
                                                  const uint32_t* __restrict__ typemask,
                                                  int stream_form, double* __restrict__ rho_out,
-                                                 double* __restrict__ u_out, int* bad) {
+                                                 double* __restrict__ u_out, int* bad, int z0) {
     using D = Dirs<Q>;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y;
-    const int z = blockIdx.z;
+    const int z = z0 + blockIdx.z;
     if (x >= g.nx) return;
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
     double f[Q];
@@ -758,6 +758,38 @@ __global__ void k_fill_eq(KGrid g, const double* __restrict__ rho, const double*
         const double cu = cu_of<Q, i>(ux, uy, uz);
         const double feq = (wt<Q, i>() * r) * (((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq);
         Store<Real>::template store<Q, i>(pdf + own + dir_off<Q, i>(g), feq);
+    });
+}
+
+// equilibrium of dense interior arrays rho (nz, ny, nx), u (nz, ny, nx, 3)
+// into the ghost-inclusive planes zg0 .. zg0 + gridDim.z - 1 of the layout;
+// a ghost cell takes the nearest interior cell's rho / u (each coordinate
+// clamped: the values fill_equilibrium_arrays gives the ghost shell, so the
+// result is bitwise that of k_fill_eq).  `shell` (optional) receives the
+// ghost cells too: the second buffer's shell (what lbm_copy_shell gives it).
+template <int Q, typename Real>
+__global__ void k_fill_eq_dense(KGrid g, const double* __restrict__ rho, const double* __restrict__ u,
+                                int zg0, Real* __restrict__ pdf, Real* __restrict__ shell) {
+    const int X = g.nx + 2;
+    const int xg = blockIdx.x * blockDim.x + threadIdx.x;
+    const int yg = blockIdx.y;
+    const int zg = zg0 + blockIdx.z;
+    if (xg >= X) return;
+    const int xi = min(max(xg - 1, 0), g.nx - 1);
+    const int yi = min(max(yg - 1, 0), g.ny - 1);
+    const int zi = min(max(zg - 1, 0), g.nz - 1);
+    const int64_t cell = ((int64_t)zi * g.ny + yi) * g.nx + xi;
+    const double r = rho[cell];
+    const double ux = u[cell * 3], uy = u[cell * 3 + 1], uz = u[cell * 3 + 2];
+    const double usq = (ux * ux + uy * uy) + uz * uz;
+    const int64_t own = lidx(g, zg - 1, 0, yg - 1, xg - 1);
+    const bool ghost = xg == 0 || xg == X - 1 || yg == 0 || yg == g.ny + 1 || zg == 0 || zg == g.nz + 1;
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        const double cu = cu_of<Q, i>(ux, uy, uz);
+        const double feq = (wt<Q, i>() * r) * (((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq);
+        Store<Real>::template store<Q, i>(pdf + own + dir_off<Q, i>(g), feq);
+        if (ghost && shell) Store<Real>::template store<Q, i>(shell + own + dir_off<Q, i>(g), feq);
     });
 }
 

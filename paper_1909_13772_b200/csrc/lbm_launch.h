@@ -15,16 +15,18 @@ struct KParams;
                       const void* src, void* dst, const uint32_t* cm, const uint32_t* tmk, int z0, \
                       int z1, cudaStream_t s);                                                   \
     cudaError_t collide_only(int q, int model, int force, const KGrid& g, const KParams& p,      \
-                             void* pdf, const uint32_t* cm, cudaStream_t s);                     \
+                             void* pdf, const uint32_t* cm, int z0, int z1, cudaStream_t s);     \
     cudaError_t stream_only(int q, const KGrid& g, const KParams& p, const void* src,            \
                             const uint32_t* cm, const uint32_t* tmk, double* out, cudaStream_t s); \
     cudaError_t moments(int q, int guo, const KGrid& g, const KParams& p, const void* src,       \
                         const uint32_t* cm, const uint32_t* tmk, int stream_form, double* rho,    \
-                        double* u, int* bad, cudaStream_t s);                                    \
+                        double* u, int* bad, int z0, int z1, cudaStream_t s);                    \
     cudaError_t convert(int q, int to_layout, const KGrid& g, double* dense, void* pdf,          \
                         cudaStream_t s);                                                         \
     cudaError_t fill_eq(int q, const KGrid& g, const double* rho, const double* u, void* pdf,    \
                         cudaStream_t s);                                                         \
+    cudaError_t fill_eq_dense(int q, const KGrid& g, const double* rho, const double* u, int zg0, \
+                              int zg1, void* pdf, void* shell, cudaStream_t s);                  \
     }
 
 LBM_DECLARE_UNIT(unit_f64)

@@ -564,6 +564,112 @@ class DeviceLattice:
         S["ev_i"].record(main)
         S["pending"] = True
 
+    # ---------------------------------------------------- pipelined job
+    def can_pipeline(self) -> bool:
+        """One rank, z not periodic: a job's sweeps can run as a wavefront
+        behind the upload (a periodic z couples the first and last planes)."""
+        return (not self.has_halo and self.box.zface_lo == _lib.ZFACE_GHOST
+                and self.box.zface_hi == _lib.ZFACE_GHOST)
+
+    def run_job(self, kp, key, masks, kp_mom, rho_h, u_h, steps, out, chunk=None):
+        """fill_equilibrium_arrays -> `steps` fused sweeps -> moments of R_K,
+        as a wavefront over chunks of z-planes so the PCIe copies overlap the
+        sweeps.  Same kernels and arithmetic as the call sequence, in another
+        order; bitwise identical results and end state.
+
+        G_n lives in buf[(c0 + n) % 2].  Step n of plane p reads G_{n-1} on
+        planes p-1..p+1 and overwrites G_{n-2} on plane p, which step n-1
+        still needs up to plane p+1: with done[n] = planes [0, done[n]) of
+        G_n finished, step n may advance to done[n-1] - 1 (to nz once step
+        n-1 is complete); the moments of R_K = S(G_{K-1}) follow step K-1
+        the same way.  Uncovered z ghost planes keep their fill values in
+        both buffers (fill writes the other buffer's shell)."""
+        b = self.box
+        nz = b.nz
+        self.join_streams()
+        main = self.stream
+        dev = self.device
+        shape_r, shape_u = (nz, b.ny, b.nx), (nz, b.ny, b.nx, 3)
+        st = getattr(self, "_job_stage", None)
+        if st is None or st["shape"] != shape_r:
+            st = {"shape": shape_r,
+                  "rho": hbm_empty(shape_r, torch.float64, dev),
+                  "u": hbm_empty(shape_u, torch.float64, dev),
+                  "rho_o": hbm_empty(shape_r, torch.float64, dev),
+                  "u_o": hbm_empty(shape_u, torch.float64, dev),
+                  "bad": torch.zeros(1, dtype=torch.int32, device=dev),
+                  "up": torch.cuda.Stream(dev), "dn": torch.cuda.Stream(dev)}
+            self._job_stage = st
+        up, dn = st["up"], st["dn"]
+        # staging reuse across jobs: uploads after the last job's fills,
+        # moments after its downloads
+        up.wait_stream(main)
+        main.wait_stream(dn)
+        st["bad"].zero_()
+        if chunk is None:
+            chunk = 32
+        chunk = max(1, min(int(chunk), nz))
+        bounds = [(z, min(z + chunk, nz)) for z in range(0, nz, chunk)]
+        evs = []
+        with torch.cuda.stream(up):
+            for z0, z1 in bounds:
+                st["rho"][z0:z1].copy_(rho_h[z0:z1], non_blocking=True)
+                st["u"][z0:z1].copy_(u_h[z0:z1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(up)
+                evs.append(ev)
+        c0 = self.cur
+        buf = self.buf
+        if masks.all_fluid:
+            cm = tm = None
+        else:
+            cm = _lib.ptr(masks.cellmask)
+            tm = _lib.ptr(masks.typemask) if masks.typed else None
+        sp = self._sp(main)
+        done = [0] * (steps + 1)
+        mdone = 0
+        launches = 0
+        for (z0, z1), ev in zip(bounds, evs):
+            main.wait_event(ev)
+            _lib.call("lbm_fill_equilibrium_planes", self.gref, _lib.ptr(st["rho"]),
+                      _lib.ptr(st["u"]), z0, z1, _lib.ptr(buf[c0]), _lib.ptr(buf[1 - c0]), sp)
+            _lib.call("lbm_collide_only_planes", self.gref, kp.ref, _lib.ptr(buf[c0]),
+                      _lib.ptr(masks.cellmask), z0, z1, sp)
+            done[0] = z1
+            for n in range(1, steps + 1):
+                lim = nz if done[n - 1] == nz else done[n - 1] - 1
+                if lim > done[n]:
+                    _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(buf[(c0 + n - 1) % 2]),
+                              _lib.ptr(buf[(c0 + n) % 2]), cm, tm, done[n], lim, sp)
+                    done[n] = lim
+                    launches += 1
+            lim = nz if done[steps - 1] == nz else done[steps - 1] - 1
+            if lim > mdone:
+                _lib.call("lbm_moments_planes", self.gref, kp_mom.ref,
+                          _lib.ptr(buf[(c0 + steps - 1) % 2]), _lib.ptr(masks.cellmask),
+                          _lib.ptr(masks.typemask), 1, mdone, lim, _lib.ptr(st["rho_o"]),
+                          _lib.ptr(st["u_o"]), _lib.ptr(st["bad"]), sp)
+                evm = torch.cuda.Event()
+                evm.record(main)
+                dn.wait_event(evm)
+                with torch.cuda.stream(dn):
+                    out[0][mdone:lim].copy_(st["rho_o"][mdone:lim], non_blocking=True)
+                    out[1][mdone:lim].copy_(st["u_o"][mdone:lim], non_blocking=True)
+                mdone = lim
+        dn.synchronize()
+        # end state: exactly what the call sequence leaves
+        self.cur = (c0 + steps) % 2
+        self.cur_kind, self.prev_kind = "G", "G"
+        self.coll_key = key
+        self.stream_masks = masks
+        self._kp_stream = kp
+        self.steps += steps
+        self.launches += launches
+        self.host_state = "device"
+        self.snapshot = None
+        self._dst_synced = None
+        return st["bad"]
+
     # ---------------------------------------------------------- readout
     def moments(self, kp, masks):
         """rho (nz,ny,nx), u (nz,ny,nx,3) of R_n on the host, fp64."""

@@ -290,7 +290,7 @@ def sweep_masks(pdf, handling):
     return masks
 
 
-def _prepare(pdf, model, force, handling):
+def _prepare(pdf, model, force, handling, upload=True):
     masks = sweep_masks(pdf, handling)
     lat = pdf.lattice
     kp, key = pdf.params(model, force, handling)
@@ -299,7 +299,7 @@ def _prepare(pdf, model, force, handling):
     if omega_key is not None:
         key = key + (("omega", _upload_rates(lat, omega_key)),)
         kp.struct.omega_cells = lat.omega_ptr
-    if lat.host_changed():
+    if upload and lat.host_changed():
         lat.upload_host()
     return lat, kp, key, masks
 
@@ -335,6 +335,51 @@ def stream_collide_n(pdf: PdfField, model, steps, *, force=None, handling=None) 
         return
     lat, kp, key, masks = _prepare(pdf, model, force, handling)
     lat.step(kp, key, masks, int(steps))
+
+
+def run_arrays(pdf: PdfField, model, steps, rho, u, *, force=None, handling=None, out=None,
+               chunk_planes=None):
+    """B200 extension: one job from host arrays to host arrays,
+        fill_equilibrium_arrays(pdf, rho, u)
+        steps x stream_collide(pdf, model, force=force, handling=handling)
+        return macroscopic_arrays(pdf, force=force, out=out)
+    with bitwise the same results and end state.  On one rank with a
+    non-periodic z axis it runs as a wavefront over chunks of z-planes
+    (DeviceLattice.run_job): the upload of later planes, the sweeps of
+    earlier ones and the download of finished ones overlap, so a job pays
+    for PCIe roughly once instead of on top of its sweeps.  `out` = (rho,
+    u) host tensors (pinned for overlap); without it host tensors are
+    allocated."""
+    import torch
+    steps = int(steps)
+    if steps < 0:
+        raise ValidationError("steps must be >= 0")
+    lat = pdf.lattice
+    b = lat.box
+    r = rho if isinstance(rho, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rho))
+    v = u if isinstance(u, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(u))
+    if tuple(r.shape) != (b.nz, b.ny, b.nx) or tuple(v.shape) != (b.nz, b.ny, b.nx, 3):
+        raise ValidationError("rho / u must cover this rank's box: "
+                              f"({b.nz}, {b.ny}, {b.nx}) and (..., 3)")
+    if steps == 0 or not lat.can_pipeline() or r.is_cuda or v.is_cuda:
+        fill_equilibrium_arrays(pdf, r, v)
+        for _ in range(steps):
+            stream_collide(pdf, model, force=force, handling=handling)
+        return macroscopic_arrays(pdf, force=force, out=out)
+    r = r.to(torch.float64).contiguous()
+    v = v.to(torch.float64).contiguous()
+    if out is None:
+        out = (torch.empty(tuple(r.shape), dtype=torch.float64),
+               torch.empty(tuple(v.shape), dtype=torch.float64))
+    # validation and parameters of the sweeps; the job replaces the whole
+    # device state, so host-side PDF data is not uploaded first
+    lat, kp, key, masks = _prepare(pdf, model, force, handling, upload=False)
+    from .collision import SRT, Guo, kernel_params as _kp
+    kp_m = _kp(pdf.stencil, SRT(1.0), force if isinstance(force, Guo) else None)
+    bad = lat.run_job(kp, key, masks, kp_m, r, v, steps, out, chunk_planes)
+    if int(bad.item()):
+        raise NumericsError(f"non-positive density {float(out[0].min())}")
+    return out
 
 
 def macroscopic_fields(pdf: PdfField, density="rho", velocity="vel", *, force=None,
