@@ -488,6 +488,11 @@ def run_e2e(args, cfg, ctx, dtype, P, forest, pdf, handling, model, force, dims)
     # job as the call sequence fill_equilibrium_arrays -> K x stream_collide
     # -> macroscopic_arrays, each phase between synchronisations)
     phases = {}
+    # (one warm pass first: the sequence uses torch copy / slice kernels that
+    # run_arrays does not, and their first launch loads modules)
+    P.fill_equilibrium_arrays(pdf, rho_h, u_h)
+    P.stream_collide(pdf, model, force=force, handling=handling)
+    P.macroscopic_arrays(pdf, force=force, out=out)
     torch.cuda.synchronize()
     t = time.perf_counter()
     P.fill_equilibrium_arrays(pdf, rho_h, u_h)

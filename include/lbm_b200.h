@@ -52,6 +52,7 @@
  *   lbm_bind_params     re-binds a parameter block's device-side state (MRT
  *                       constant tables) before a captured CUDA graph replays.
  *   lbm_fill_equilibrium_planes / lbm_collide_only_planes / lbm_moments_planes
+ *   lbm_fill_collide_planes
  *                       the same three steps on a range of z-planes, for a
  *                       pipelined job (fill_equilibrium -> K x stream_collide
  *                       -> macroscopic, sweep.py:51-183) whose host<->device
@@ -305,6 +306,12 @@ int lbm_fill_equilibrium(const lbm_grid_t* g, const double* rho,
 int lbm_fill_equilibrium_planes(const lbm_grid_t* g, const double* rho,
                                 const double* u, int z0, int z1, void* pdf,
                                 void* pdf_shell, void* stream);
+/* fill_planes followed by collide_only_planes in one pass (interior fluid
+ * cells stored collided, G_0 = C(R_0); bitwise the two calls). */
+int lbm_fill_collide_planes(const lbm_grid_t* g, const lbm_params_t* p,
+                            const double* rho, const double* u, int z0,
+                            int z1, void* pdf, void* pdf_shell,
+                            const uint32_t* cellmask, void* stream);
 int lbm_collide_only_planes(const lbm_grid_t* g, const lbm_params_t* p,
                             void* pdf, const uint32_t* cellmask, int z0,
                             int z1, void* stream);

@@ -939,6 +939,29 @@ int lbm_fill_equilibrium_planes(const lbm_grid_t* g, const double* rho, const do
     return cuda_status(e, "lbm_fill_equilibrium_planes");
 }
 
+int lbm_fill_collide_planes(const lbm_grid_t* g, const lbm_params_t* p, const double* rho,
+                            const double* u, int z0, int z1, void* pdf, void* pdf_shell,
+                            const uint32_t* cellmask, void* stream) {
+    KGrid k;
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
+    if (!rho || !u || !pdf || !cellmask) return fail(LBM_EINVAL, "NULL buffer");
+    if (pdf == pdf_shell) return fail(LBM_EINVAL, "pdf_shell must be the other field");
+    if (z0 < 0 || z1 > g->nz || z0 > z1) return fail(LBM_EINVAL, "bad plane range [%d, %d)", z0, z1);
+    if (z0 == z1) return LBM_OK;
+    const int zg0 = z0 == 0 ? 0 : z0 + 1;
+    const int zg1 = z1 == g->nz ? g->nz + 2 : z1 + 1;
+    cudaError_t e = g->real_bytes == 8
+                        ? unit_f64::fill_collide(g->q, p->model, p->force_mode, k, kp, rho, u, zg0,
+                                                 zg1, pdf, pdf_shell, cellmask, s)
+                        : unit_f32::fill_collide(g->q, p->model, p->force_mode, k, kp, rho, u, zg0,
+                                                 zg1, pdf, pdf_shell, cellmask, s);
+    return cuda_status(e, "lbm_fill_collide_planes");
+}
+
 int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags, const uint32_t bits[5],
                        uint32_t* cellmask, uint32_t* typemask, int* err, void* stream) {
     KGrid k;

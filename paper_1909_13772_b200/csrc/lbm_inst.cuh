@@ -368,5 +368,23 @@ cudaError_t fill_eq_dense(int q, const KGrid& g, const double* rho, const double
     });
 }
 
+cudaError_t fill_collide(int q, int model, int force, const KGrid& g, const KParams& p,
+                         const double* rho, const double* u, int zg0, int zg1, void* pdf,
+                         void* shell, const uint32_t* cm, cudaStream_t s) {
+    if (zg1 <= zg0) return cudaSuccess;
+    if (model == LBM_SRT_FIELD) model = 4;
+    else if (model == LBM_MRT && p.mrt_fast) model = 3;
+    return by_q(q, [&](auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        return by_model<Q>(model, force, [&](auto Mc, auto Fc) {
+            dim3 b = cell_block(g.nx + 2);
+            dim3 grid((g.nx + 2 + b.x - 1) / b.x, g.ny + 2, zg1 - zg0);
+            k_fill_collide<Q, LBM_REAL, decltype(Mc)::value, decltype(Fc)::value>
+                <<<grid, b, 0, s>>>(g, p, rho, u, zg0, (LBM_REAL*)pdf, (LBM_REAL*)shell, cm);
+            return cudaGetLastError();
+        });
+    });
+}
+
 }  // namespace LBM_UNIT
 }  // namespace lbm

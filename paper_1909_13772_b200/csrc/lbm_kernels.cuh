@@ -793,4 +793,56 @@ __global__ void k_fill_eq_dense(KGrid g, const double* __restrict__ rho, const d
     });
 }
 
+// k_fill_eq_dense followed by k_collide_only in one pass (a pipelined job's
+// first touch of a plane chunk): interior fluid cells are collided before
+// they are stored (G_0 = C(R_0)), every other cell keeps R_0; ghost cells
+// also go to `shell`.  The collision starts from the STORED representation
+// of feq (fp32: the centred float), so the result is bitwise that of the two
+// separate passes.
+template <int Q, typename Real, int MODEL, int FORCE>
+__global__ void __launch_bounds__(128) k_fill_collide(KGrid g, KParams p, const double* __restrict__ rho,
+                                                      const double* __restrict__ u, int zg0,
+                                                      Real* __restrict__ pdf, Real* __restrict__ shell,
+                                                      const uint32_t* __restrict__ cellmask) {
+    const int X = g.nx + 2;
+    const int xg = blockIdx.x * blockDim.x + threadIdx.x;
+    const int yg = blockIdx.y;
+    const int zg = zg0 + blockIdx.z;
+    if (xg >= X) return;
+    const int xi = min(max(xg - 1, 0), g.nx - 1);
+    const int yi = min(max(yg - 1, 0), g.ny - 1);
+    const int zi = min(max(zg - 1, 0), g.nz - 1);
+    const int64_t cell = ((int64_t)zi * g.ny + yi) * g.nx + xi;
+    const double r = rho[cell];
+    const double ux = u[cell * 3], uy = u[cell * 3 + 1], uz = u[cell * 3 + 2];
+    const double usq = (ux * ux + uy * uy) + uz * uz;
+    const int64_t own = lidx(g, zg - 1, 0, yg - 1, xg - 1);
+    const bool ghost = xg == 0 || xg == X - 1 || yg == 0 || yg == g.ny + 1 || zg == 0 || zg == g.nz + 1;
+    using Acc = AccOf<Real>;
+    Acc f[Q];
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        const double cu = cu_of<Q, i>(ux, uy, uz);
+        const double feq = (wt<Q, i>() * r) * (((1.0 + 3.0 * cu) + (4.5 * cu) * cu) - 1.5 * usq);
+        if constexpr (std::is_same_v<Acc, double>) {
+            f[i] = feq;
+        } else {
+            f[i] = (float)(feq - wt<Q, i>());   // Store<float>::store's rounding
+        }
+    });
+    if (ghost) {
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            store_any<Q, i>(pdf + own + dir_off<Q, i>(g), f[i]);
+            if (shell) store_any<Q, i>(shell + own + dir_off<Q, i>(g), f[i]);
+        });
+        return;
+    }
+    if (cellmask[cell] & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p, cell);
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        store_any<Q, i>(pdf + own + dir_off<Q, i>(g), f[i]);
+    });
+}
+
 }  // namespace lbm

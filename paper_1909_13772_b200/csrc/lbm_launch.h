@@ -27,6 +27,9 @@ struct KParams;
                         cudaStream_t s);                                                         \
     cudaError_t fill_eq_dense(int q, const KGrid& g, const double* rho, const double* u, int zg0, \
                               int zg1, void* pdf, void* shell, cudaStream_t s);                  \
+    cudaError_t fill_collide(int q, int model, int force, const KGrid& g, const KParams& p,      \
+                             const double* rho, const double* u, int zg0, int zg1, void* pdf,    \
+                             void* shell, const uint32_t* cm, cudaStream_t s);                   \
     }
 
 LBM_DECLARE_UNIT(unit_f64)

@@ -607,7 +607,8 @@ class DeviceLattice:
         main.wait_stream(dn)
         st["bad"].zero_()
         if chunk is None:
-            chunk = 32
+            import os
+            chunk = int(os.environ.get("LBM_B200_JOB_CHUNK", "32"))
         chunk = max(1, min(int(chunk), nz))
         bounds = [(z, min(z + chunk, nz)) for z in range(0, nz, chunk)]
         evs = []
@@ -631,10 +632,11 @@ class DeviceLattice:
         launches = 0
         for (z0, z1), ev in zip(bounds, evs):
             main.wait_event(ev)
-            _lib.call("lbm_fill_equilibrium_planes", self.gref, _lib.ptr(st["rho"]),
-                      _lib.ptr(st["u"]), z0, z1, _lib.ptr(buf[c0]), _lib.ptr(buf[1 - c0]), sp)
-            _lib.call("lbm_collide_only_planes", self.gref, kp.ref, _lib.ptr(buf[c0]),
-                      _lib.ptr(masks.cellmask), z0, z1, sp)
+            # equilibrium + G_0 = C(R_0) of the chunk in one pass (the other
+            # buffer gets the ghost shell)
+            _lib.call("lbm_fill_collide_planes", self.gref, kp.ref, _lib.ptr(st["rho"]),
+                      _lib.ptr(st["u"]), z0, z1, _lib.ptr(buf[c0]), _lib.ptr(buf[1 - c0]),
+                      _lib.ptr(masks.cellmask), sp)
             done[0] = z1
             for n in range(1, steps + 1):
                 lim = nz if done[n - 1] == nz else done[n - 1] - 1
