@@ -259,6 +259,11 @@ int lbm_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
 int lbm_ipc_open(const void* handle, void** base_out);
 int lbm_ipc_close(void* base);
 int lbm_stream_wait(const void* flag, uint32_t value, void* stream);
+/* 1 if the current device can flush remote writes after a stream wait
+ * (CU_STREAM_WAIT_VALUE_FLUSH: a peer's halo stores are visible once its
+ * later flag write is).  Without it the fused halo between GPUs is not used
+ * (halo.select_transport falls back to NCCL send/recv). */
+int lbm_can_flush_remote_writes(void);
 
 /* Collide, in place, every interior cell whose cellmask has LBM_MASK_FLUID
  * (G_0 = C(R_0)). */

@@ -34,7 +34,7 @@ EXPORTS = (
     "lbm_bind_params", "lbm_slot_collide", "lbm_slot_stream_pull", "lbm_refresh_fluid_mask",
     "lbm_map_spheres", "lbm_copy_shell", "lbm_slot_apply_links",
     "lbm_fill_equilibrium_planes", "lbm_collide_only_planes", "lbm_moments_planes",
-    "lbm_fill_collide_planes",
+    "lbm_fill_collide_planes", "lbm_can_flush_remote_writes",
 )
 
 
@@ -123,6 +123,7 @@ def load(path: Path | None = None):
         "lbm_collide_only_planes": ([G, PR, P, P, I, I, P], I),
         "lbm_moments_planes": ([G, PR, P, P, P, I, I, I, P, P, P, P], I),
         "lbm_fill_collide_planes": ([G, PR, P, P, I, I, P, P, P, P], I),
+        "lbm_can_flush_remote_writes": ([], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

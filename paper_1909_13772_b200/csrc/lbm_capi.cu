@@ -795,6 +795,14 @@ int lbm_stream_signal(void* flag, uint32_t value, void* stream) {
     return LBM_OK;
 }
 
+int lbm_can_flush_remote_writes(void) {
+    int dev = 0, flush = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, dev) != cudaSuccess)
+        return 0;
+    return flush ? 1 : 0;
+}
+
 int lbm_stream_wait(const void* flag, uint32_t value, void* stream) {
     if (!flag) return fail(LBM_EINVAL, "flag is NULL");
     int st = memops_init();

@@ -1,4 +1,5 @@
-"""Per-step z-face halo exchange of the G-form, zero-copy over NCCL.
+"""Per-step z-face halo exchange of the G-form: fused peer stores over
+NVLink (PeerHalo, the default between GPUs) or NCCL send/recv in place.
 
 Replaces the per-step `exchange_ghosts(forest, [GhostPackInfo("pdf")])`
 of stream_collide (lbm/sweep.py:110-114, field/ghost.py:202-264).  Because
@@ -393,6 +394,13 @@ def select_transport(lat) -> str:
     can_map = all(ctx.all_gather(bool(can_map)).values())
     if backend == "nccl":
         if want == "nccl" or shared or not can_map:
+            return "nccl"
+        # a peer GPU's halo stores and its later flag write may be reordered
+        # on arrival unless the stream wait can flush remote writes
+        # (CU_STREAM_WAIT_VALUE_FLUSH): without it, send/recv
+        with torch.cuda.device(idx):
+            flush = bool(_lib.load().lbm_can_flush_remote_writes())
+        if not all(ctx.all_gather(flush).values()):
             return "nccl"
         return "peer-device"
     # gloo on CUDA tensors: host-staged unless the fused transport is asked for
