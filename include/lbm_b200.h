@@ -28,6 +28,8 @@
  *                       (field/core.py:34-70; "fzyx" raw shape (q,Z,Y,X)).
  *   lbm_build_cellmask  build_index_lists + sweep-time flag validation
  *                       (lbm/boundary.py:48-97, lbm/sweep.py:124-136).
+ *   lbm_build_linkbits / lbm_fused_step_bits  the same link lists as one
+ *                       bit per cell for NoSlip-only lattices (ABI 7).
  *   lbm_map_spheres     map_bodies' voxeliser (coupling/mapping.py:100-140).
  *   lbm_refresh_fluid_mask  the per-sweep fluid mask of flags edited after
  *                       freeze() (lbm/sweep.py:124-136; links stay frozen).
@@ -85,7 +87,7 @@
 extern "C" {
 #endif
 
-#define LBM_B200_ABI_VERSION 6
+#define LBM_B200_ABI_VERSION 7
 
 /* status codes */
 #define LBM_OK 0
@@ -219,6 +221,17 @@ int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p,
                    const uint32_t* typemask, int z_begin, int z_end,
                    void* stream);
 
+/* lbm_fused_step reading the link-bit map (ABI 7) instead of the 4 B/cell
+ * cell mask where the launched kernel can: linkbits from lbm_build_linkbits
+ * (0 mismatches) for the same cellmask, typemask = NULL, no moving-body
+ * walls.  Other launches (and linkbits = NULL) read cellmask as
+ * lbm_fused_step does, so the result never depends on the choice.
+ * LBM_B200_LINKBITS=0 in the environment forces the cell mask (A/B runs). */
+int lbm_fused_step_bits(const lbm_grid_t* g, const lbm_params_t* p,
+                        const void* src, void* dst, const uint32_t* cellmask,
+                        const uint32_t* typemask, const uint64_t* linkbits,
+                        int z_begin, int z_end, void* stream);
+
 /* lbm_fused_step plus the fused z-face halo (ABI 4): the plane z = 0 also
  * stores its c_z = -1 directions into peer_lo, the plane z = nz-1 its
  * c_z = +1 directions into peer_hi, at the same (slot, y, x) offsets.  A peer
@@ -335,6 +348,22 @@ int lbm_moments_planes(const lbm_grid_t* g, const lbm_params_t* p,
  * Pressure links, [7] first fluid cell pulling from an uncovered Fluid
  * ghost + 1 (unsupported: such ghosts would collide every step in the
  * reference but are never refreshed).  Linear indices are z*ny*nx + y*nx + x (interior). */
+/* Link-bit map (ABI 7): one bit per ghost-inclusive cell, N(c) = "c is not
+ * collided and a fluid cell pulling from it takes a NoSlip link", stored as
+ * (nz+2) (ny+2) ceil(nx/32) uint64 words (word w of a row = cells
+ * 32w .. 32w+63, consecutive words overlap by 32 cells).  The cell mask of a
+ * NoSlip-only lattice is a function of it: code(x) = 0 if N(x), else
+ * LBM_MASK_FLUID | sum_i N(x - c_i) << i.  lbm_build_linkbits derives the map
+ * from a cellmask and checks that derivation on every interior cell:
+ * *mismatch (device int, set to INT_MAX by the caller) receives 1 + the first
+ * cell whose code the map does not reproduce (typed links, flags edited after
+ * freeze(), ...); the map may be used only when it stays INT_MAX.
+ * Same setup role as lbm_build_cellmask (build_index_lists,
+ * lbm/boundary.py:48-97). */
+int64_t lbm_linkbits_words(const lbm_grid_t* g);
+int lbm_build_linkbits(const lbm_grid_t* g, const uint32_t* cellmask, uint64_t* linkbits,
+                       int* mismatch, void* stream);
+
 int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags,
                        const uint32_t bits[5], uint32_t* cellmask,
                        uint32_t* typemask, int* err, void* stream);

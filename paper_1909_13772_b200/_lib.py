@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
 
 LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
 ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
-ABI_VERSION = 6
+ABI_VERSION = 7
 SRT, TRT, MRT, SRT_FIELD = 0, 1, 2, 3
 MASK_FLUID = 0x1
 MASK_UBB = 0x80000000
@@ -35,6 +35,7 @@ EXPORTS = (
     "lbm_map_spheres", "lbm_copy_shell", "lbm_slot_apply_links",
     "lbm_fill_equilibrium_planes", "lbm_collide_only_planes", "lbm_moments_planes",
     "lbm_fill_collide_planes", "lbm_can_flush_remote_writes",
+    "lbm_fused_step_bits", "lbm_linkbits_words", "lbm_build_linkbits",
 )
 
 
@@ -124,6 +125,9 @@ def load(path: Path | None = None):
         "lbm_moments_planes": ([G, PR, P, P, P, I, I, I, P, P, P, P], I),
         "lbm_fill_collide_planes": ([G, PR, P, P, I, I, P, P, P, P], I),
         "lbm_can_flush_remote_writes": ([], I),
+        "lbm_fused_step_bits": ([G, PR, P, P, P, P, P, I, I, P], I),
+        "lbm_linkbits_words": ([G], I64),
+        "lbm_build_linkbits": ([G, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -284,6 +284,7 @@ def _combined_masks(lat, static, owner_box):
     _lib.call("lbm_build_moving_masks", lat.gref, _lib.ptr(static.cellmask), _lib.ptr(owner_t),
               _lib.ptr(cm), _lib.ptr(lm), _lib.ptr(n), lat._sp())
     masks = Masks(cm, static.typemask, dict(static.counts), static.unflagged_cell)
+    masks.bits_ok = False   # moving-wall links need the full mask
     masks.n_moving = int(n.item())
     masks.static = static
     lat._moving_masks = (tag, masks, owner_t, lm)

@@ -587,6 +587,47 @@ dim3 cell_block(int nx) { return dim3(nx >= 128 ? 128 : ((nx + 31) / 32) * 32, 1
 }  // namespace
 
 // ================================================================== C-ABI
+// ------------------------------------------------------- link-bit map
+// (layout and rule: code_from_bits in lbm_kernels.cuh)
+__device__ __forceinline__ void set_bit(const KGrid& g, uint64_t* bits, int xg, int yg, int zg) {
+    const int64_t bw = (g.nx + 31) >> 5;
+    const int64_t row = ((int64_t)zg * (g.ny + 2) + yg) * bw;
+    const int w = xg >> 5;
+    if (w < bw) atomicOr((unsigned long long*)(bits + row + w), 1ull << (xg & 31));
+    if (w >= 1 && w - 1 < bw) atomicOr((unsigned long long*)(bits + row + w - 1), 1ull << ((xg & 31) + 32));
+}
+
+// N of every interior cell from its own code; N of ghost cells from the
+// links that pull from them
+template <int Q>
+__global__ void k_linkbits_set(KGrid g, const uint32_t* __restrict__ cellmask, uint64_t* bits) {
+    using D = Dirs<Q>;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const uint32_t code = cellmask[((int64_t)z * g.ny + y) * g.nx + x];
+    if (!(code & LBM_MASK_FLUID)) set_bit(g, bits, x + 1, y + 1, z + 1);
+    static_for<1, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        const int xs = x - D::cx[i], ys = y - D::cy[i], zs = z - D::cz[i];
+        const bool ghost = xs < 0 || xs >= g.nx || ys < 0 || ys >= g.ny || zs < 0 || zs >= g.nz;
+        if (ghost && ((code >> i) & 1u)) set_bit(g, bits, xs + 1, ys + 1, zs + 1);
+    });
+}
+
+// every interior cell: the derived code must equal the mask bit for bit
+template <int Q>
+__global__ void k_linkbits_check(KGrid g, const uint32_t* __restrict__ cellmask,
+                                 const uint64_t* __restrict__ bits, int* mismatch) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x >= g.nx) return;
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    if (code_from_bits<Q>(g, bits, x, y, z) != cellmask[cell]) atomicMin(mismatch, (int)(cell + 1 < 0x7fffffff ? cell + 1 : 0x7fffffff));
+}
+
 extern "C" {
 
 int lbm_abi_version(void) { return LBM_B200_ABI_VERSION; }
@@ -639,6 +680,12 @@ int lbm_face_span(const lbm_grid_t* g, int face, int64_t* send_off, int64_t* rec
 int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p, const void* src, void* dst,
                    const uint32_t* cellmask, const uint32_t* typemask, int z_begin, int z_end,
                    void* stream) {
+    return lbm_fused_step_bits(g, p, src, dst, cellmask, typemask, nullptr, z_begin, z_end, stream);
+}
+
+int lbm_fused_step_bits(const lbm_grid_t* g, const lbm_params_t* p, const void* src, void* dst,
+                        const uint32_t* cellmask, const uint32_t* typemask,
+                        const uint64_t* linkbits, int z_begin, int z_end, void* stream) {
     KGrid k;
     KParams kp;
     cudaStream_t s = (cudaStream_t)stream;
@@ -651,9 +698,9 @@ int lbm_fused_step(const lbm_grid_t* g, const lbm_params_t* p, const void* src, 
         return fail(LBM_EINVAL, "plane range [%d, %d) outside 0..%d", z_begin, z_end, g->nz);
     cudaError_t e = g->real_bytes == 8
                         ? unit_f64::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
-                                          typemask, z_begin, z_end, s)
+                                          typemask, linkbits, z_begin, z_end, s)
                         : unit_f32::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
-                                          typemask, z_begin, z_end, s);
+                                          typemask, linkbits, z_begin, z_end, s);
     return cuda_status(e, "lbm_fused_step");
 }
 
@@ -679,9 +726,9 @@ int lbm_fused_step_peer(const lbm_grid_t* g, const lbm_params_t* p, const void* 
     kp.peer_hi = peer_hi;
     cudaError_t e = g->real_bytes == 8
                         ? unit_f64::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
-                                          typemask, z_begin, z_end, s)
+                                          typemask, nullptr, z_begin, z_end, s)
                         : unit_f32::fused(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
-                                          typemask, z_begin, z_end, s);
+                                          typemask, nullptr, z_begin, z_end, s);
     return cuda_status(e, "lbm_fused_step_peer");
 }
 
@@ -986,6 +1033,33 @@ int lbm_build_cellmask(const lbm_grid_t* g, const uint32_t* flags, const uint32_
         return cudaGetLastError();
     });
     return cuda_status(e, "lbm_build_cellmask");
+}
+
+int64_t lbm_linkbits_words(const lbm_grid_t* g) {
+    KGrid k;
+    if (check_grid(g, &k) != LBM_OK) return -1;
+    return (int64_t)(g->nz + 2) * (g->ny + 2) * ((g->nx + 31) / 32);
+}
+
+int lbm_build_linkbits(const lbm_grid_t* g, const uint32_t* cellmask, uint64_t* linkbits,
+                       int* mismatch, void* stream) {
+    KGrid k;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if (!cellmask || !linkbits || !mismatch) return fail(LBM_EINVAL, "NULL buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t words = (int64_t)(g->nz + 2) * (g->ny + 2) * ((g->nx + 31) / 32);
+    cudaError_t e = cudaMemsetAsync(linkbits, 0, (size_t)words * sizeof(uint64_t), s);
+    if (e != cudaSuccess) return cuda_status(e, "lbm_build_linkbits");
+    dim3 blk = cell_block(g->nx);
+    dim3 grid((g->nx + blk.x - 1) / blk.x, g->ny, g->nz);
+    e = by_q(g->q, [&](auto Qc) {
+        constexpr int Q = decltype(Qc)::value;
+        k_linkbits_set<Q><<<grid, blk, 0, s>>>(k, cellmask, linkbits);
+        k_linkbits_check<Q><<<grid, blk, 0, s>>>(k, cellmask, linkbits, mismatch);
+        return cudaGetLastError();
+    });
+    return cuda_status(e, "lbm_build_linkbits");
 }
 
 int lbm_map_spheres(int n_blocks, const int32_t cells[3], const double* frame, const int32_t* first,

@@ -166,10 +166,25 @@ cudaError_t fused_vec_t(const KGrid& g, const KParams& p, const void* src, void*
 }
 #endif  // LBM_VEC_VARIANT
 
+// launches that may read the link-bit map instead of the cell mask: D3Q19
+// SRT / TRT (configs 0, 1, 3, 4) and the factorised D3Q27 MRT, NoSlip-only
+// (no typemask), no moving walls, no fused halo
+template <int Q, int MODEL, int FORCE>
+constexpr bool bits_variant() {
+    return (Q == 19 && MODEL <= 1 && FORCE != 2) || (Q == 27 && MODEL == 3);
+}
+
+inline bool use_bits() {
+    const char* e = getenv("LBM_B200_LINKBITS");
+    return !(e && e[0] == '0');
+}
+
 template <int Q, int MODEL, int FORCE>
 cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst,
-                    const uint32_t* cm, const uint32_t* tmk, int z0, int z1, cudaStream_t s) {
+                    const uint32_t* cm, const uint32_t* tmk, const uint64_t* lb, int z0, int z1,
+                    cudaStream_t s) {
     if (z1 <= z0) return cudaSuccess;
+    const bool bits = lb && cm && !tmk && !p.mv_link && !p.peer_lo && !p.peer_hi && use_bits();
     // TMA staging for the 3-D SRT / TRT / factorised-MRT sweeps (the dense
     // MRT tables and SimpleShift keep the LDG kernel)
 #ifdef LBM_VEC_VARIANT
@@ -195,8 +210,19 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
     if constexpr (std::is_same_v<LBM_REAL, float> && Q == 19 && (MODEL == 0 || MODEL == 1)) {
         if (!p.mv_link && !peer && !tmk && use_z2()) {
             dim3 grid2(grid.x, grid.y, (z1 - z0 + 1) / 2);
-            k_fused_z2<Q, LBM_REAL, MODEL, FORCE, false><<<grid2, b, 0, s>>>(
-                g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0, z1);
+            if (bits)
+                k_fused_z2<Q, LBM_REAL, MODEL, FORCE, false, true><<<grid2, b, 0, s>>>(
+                    g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, (const uint32_t*)lb, nullptr, z0, z1);
+            else
+                k_fused_z2<Q, LBM_REAL, MODEL, FORCE, false><<<grid2, b, 0, s>>>(
+                    g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0, z1);
+            return cudaGetLastError();
+        }
+    }
+    if constexpr (bits_variant<Q, MODEL, FORCE>()) {
+        if (bits) {
+            k_fused<Q, LBM_REAL, MODEL, FORCE, false, false, true><<<grid, b, 0, s>>>(
+                g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, (const uint32_t*)lb, nullptr, z0);
             return cudaGetLastError();
         }
     }
@@ -276,15 +302,15 @@ cudaError_t by_q(int q, F&& fn) {
 namespace LBM_UNIT {
 
 cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p, const void* src,
-                  void* dst, const uint32_t* cm, const uint32_t* tmk, int z0, int z1,
-                  cudaStream_t s) {
+                  void* dst, const uint32_t* cm, const uint32_t* tmk, const uint64_t* lb, int z0,
+                  int z1, cudaStream_t s) {
     if (model == LBM_SRT_FIELD) model = 4;
     else if (model == LBM_MRT && p.mrt_fast && !p.mv_link) model = 3;  // moving walls: dense MRT
     return by_q(q, [&](auto Qc) {
         constexpr int Q = decltype(Qc)::value;
         return by_model<Q>(model, force, [&](auto Mc, auto Fc) {
-            return fused_t<Q, decltype(Mc)::value, decltype(Fc)::value>(g, p, src, dst, cm, tmk, z0,
-                                                                        z1, s);
+            return fused_t<Q, decltype(Mc)::value, decltype(Fc)::value>(g, p, src, dst, cm, tmk, lb,
+                                                                        z0, z1, s);
         });
     });
 }

@@ -119,6 +119,69 @@ __device__ __forceinline__ void prefetch_mask(const KGrid& g, const uint32_t* ce
     }
 }
 
+// ---------------------------------------------------------------- link bits
+// A NoSlip-only lattice's cell mask is a function of one bit per cell: with
+// N(c) = "c is not collided and a fluid neighbour pulling from it takes a
+// bounce-back link", code(x) = 0 if N(x), else FLUID | sum_i N(x - c_i) << i.
+// The link-bit map (lbm_build_linkbits) stores N over the ghost-inclusive box
+// as uint64 words [(zg * (ny + 2) + yg) * bw + w], bw = ceil(nx / 32): bit b of
+// word w is cell xg = 32 w + b.  Consecutive words overlap by 32 cells, so the
+// 34 cells a warp of 32 reads (x - 1 .. x + 32) sit in ONE word per row and
+// every lane of the warp loads the same address (one broadcast per row).  At
+// 512^3 the map is 34 MB (0.25 B per cell) against the 4 B/cell mask; the
+// map is built only when the derivation reproduces the full mask on every
+// cell (typed links, flags edited after freeze() etc. keep the mask).
+template <int Q>
+constexpr bool bits_row_used(int dz, int dy) {
+    for (int i = 0; i < Q; ++i)
+        if (-Dirs<Q>::cz[i] == dz && -Dirs<Q>::cy[i] == dy) return true;
+    return false;
+}
+
+// link-bit words are re-read by the rows y +- 1 / planes z +- 1 of the sweep,
+// about two planes of field traffic later: keep them in L2 (evict_last)
+__device__ __forceinline__ uint64_t ldg_bits(const uint64_t* p) {
+    uint64_t v;
+    asm("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+        "ld.global.nc.L2::cache_hint.u64 %0, [%1], pol;\n}" : "=l"(v) : "l"(p));
+    return v;
+}
+
+template <int Q>
+__device__ __forceinline__ uint32_t code_from_bits(const KGrid& g, const uint64_t* __restrict__ bits,
+                                                   int x, int y, int z) {
+    using D = Dirs<Q>;
+    const int64_t bw = (g.nx + 31) >> 5;
+    const int64_t ps = (int64_t)(g.ny + 2) * bw;
+    const uint64_t* c = bits + ((int64_t)(z + 1) * (g.ny + 2) + (y + 1)) * bw + (x >> 5);
+    const int l = x & 31;
+    uint32_t w[3][3];
+    static_for<0, 9>([&](auto R_) {
+        constexpr int r = decltype(R_)::value;
+        constexpr int dz = r / 3 - 1, dy = r % 3 - 1;
+        if constexpr (bits_row_used<Q>(dz, dy))
+            w[dz + 1][dy + 1] = (uint32_t)(ldg_bits(c + dz * ps + dy * bw) >> l) & 7u;
+        else
+            w[dz + 1][dy + 1] = 0u;
+    });
+    if (w[1][1] & 2u) return 0u;
+    uint32_t code = LBM_MASK_FLUID;
+    static_for<1, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        constexpr int dz = -D::cz[i], dy = -D::cy[i], b = 1 - D::cx[i];
+        code |= ((w[dz + 1][dy + 1] >> b) & 1u) << i;
+    });
+    return code;
+}
+
+// the cell code a fused kernel works with: full mask, link bits or none
+template <int Q, bool BITS>
+__device__ __forceinline__ uint32_t cell_code(const KGrid& g, const uint32_t* __restrict__ cellmask,
+                                              int x, int y, int z, int64_t cell) {
+    if constexpr (BITS) return code_from_bits<Q>(g, reinterpret_cast<const uint64_t*>(cellmask), x, y, z);
+    else return cellmask ? __ldg(cellmask + cell) : LBM_MASK_FLUID;
+}
+
 // (Measured and dropped: L2::128B / L2::256B prefetch-size qualifiers on the
 // pulls - within noise on configs 4 fp64 / fp32 and 2.)
 // (Measured and dropped: choosing the keep policy per warp - any wall lane
@@ -503,7 +566,9 @@ constexpr int fused_minb_bx() {
 // (Measured and rejected: visiting rows in tiles of 8..64 rows, all planes of
 // a tile first, to bring the z-neighbour that re-reads a bounce-back source
 // closer in time: -1..-8 % on configs 4 fp64 / fp32 and 2.)
-template <int Q, typename Real, int MODEL, int FORCE, bool MOVING = false, bool PEER = false>
+// BITS: `cellmask` is a link-bit map (code_from_bits), not the 4 B/cell mask.
+template <int Q, typename Real, int MODEL, int FORCE, bool MOVING = false, bool PEER = false,
+          bool BITS = false>
 __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FORCE>())
     k_fused(KGrid g, KParams p, const Real* __restrict__ src,
                                                Real* __restrict__ dst,
@@ -522,8 +587,8 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FO
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
     // cellmask == NULL: every cell fluid, no links (periodic runs without a
     // boundary handling) - saves the 4 B/cell mask read
-    const uint32_t code = cellmask ? __ldg(cellmask + cell) : LBM_MASK_FLUID;
-    prefetch_mask(g, cellmask, cell, (int64_t)g.nx * g.ny * g.nz);
+    const uint32_t code = cell_code<Q, BITS>(g, cellmask, x, y, z, cell);
+    if constexpr (!BITS) prefetch_mask(g, cellmask, cell, (int64_t)g.nx * g.ny * g.nz);
     using Acc = AccOf<Real>;
     Acc f[Q];
     pull_cell<Q, Real, Acc, MOVING ? 2 : 0>(g, p, src, x, y, z, code, typemask, generic, f);
@@ -577,7 +642,7 @@ __device__ __forceinline__ bool plane_wraps(const KGrid& g, int z) {
     return (g.zlo == LBM_ZFACE_WRAP && z == 0) || (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1);
 }
 
-template <int Q, typename Real, int MODEL, int FORCE, bool TYPED>
+template <int Q, typename Real, int MODEL, int FORCE, bool TYPED, bool BITS = false>
 __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FORCE>())
     k_fused_z2(KGrid g, KParams p, const Real* __restrict__ src, Real* __restrict__ dst,
                const uint32_t* __restrict__ cellmask, const uint32_t* __restrict__ typemask,
@@ -592,10 +657,9 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FO
     if (x >= g.nx) return;
     const int64_t plane_cells = (int64_t)g.ny * g.nx;
     const int64_t cell_a = ((int64_t)za * g.ny + y) * g.nx + x;
-    const uint32_t code_a = cellmask ? __ldg(cellmask + cell_a) : LBM_MASK_FLUID;
-    const uint32_t code_b = !two ? 0u : cellmask ? __ldg(cellmask + cell_a + plane_cells)
-                                                 : LBM_MASK_FLUID;
-    {   // both planes of the pair, (link_hint >> 1) pair-rows ahead; a row
+    const uint32_t code_a = cell_code<Q, BITS>(g, cellmask, x, y, za, cell_a);
+    const uint32_t code_b = !two ? 0u : cell_code<Q, BITS>(g, cellmask, x, y, za + 1, cell_a + plane_cells);
+    if constexpr (!BITS) {   // both planes of the pair, (link_hint >> 1) pair-rows ahead; a row
         // index beyond ny continues in the next plane pair
         const int64_t ncells = (int64_t)g.nx * g.ny * g.nz;
         const int64_t c = (g.link_hint >> 1) > g.ny - 1 - y ? cell_a + plane_cells : cell_a;

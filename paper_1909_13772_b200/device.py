@@ -148,6 +148,27 @@ class Masks:
         self.counts = counts          # dict NoSlip/UBB/Pressure -> links on this rank
         self.unflagged_cell = unflagged_cell
         self.all_fluid = all_fluid    # the fused step may skip the mask (NULL)
+        self.bits_ok = True           # worth deriving a link-bit map (not moving-wall masks)
+        self._linkbits = None         # uint64 map, or False when the derivation fails
+
+    def linkbits(self, lat):
+        """Device pointer of the link-bit map that reproduces this cell mask
+        (lbm_build_linkbits: 1 bit per cell instead of 4 bytes for the fused
+        sweep), or None where it does not apply: no mask, typed (UBB /
+        Pressure) links, moving walls, or a mask the bits cannot express
+        (flags edited after freeze()).  Built once per mask, checked on the
+        device on every cell (one sync, at setup)."""
+        if self.all_fluid or self.typed or not self.bits_ok:
+            return None
+        if self._linkbits is None:
+            n = int(_lib.load().lbm_linkbits_words(lat.gref))
+            bits = torch.empty(max(n, 1), dtype=torch.int64, device=self.cellmask.device)
+            big = np.iinfo(np.int32).max
+            mismatch = torch.full((1,), big, dtype=torch.int32, device=self.cellmask.device)
+            _lib.call("lbm_build_linkbits", lat.gref, _lib.ptr(self.cellmask), _lib.ptr(bits),
+                      _lib.ptr(mismatch), lat._sp())
+            self._linkbits = bits if int(mismatch.item()) == big else False
+        return _lib.ptr(self._linkbits) if self._linkbits is not False else None
 
     @property
     def typed(self) -> bool:
@@ -467,10 +488,11 @@ class DeviceLattice:
         self.ensure_collided(kp, key, masks)
         nz = self.box.nz
         if masks.all_fluid:
-            cm = tm = None      # fused step reads no mask bytes
+            cm = tm = lb = None      # fused step reads no mask bytes
         else:
             cm = _lib.ptr(masks.cellmask)
             tm = _lib.ptr(masks.typemask) if masks.typed else None
+            lb = masks.linkbits(self)
         lib = _lib.load()
         main = self.stream
         if self.has_halo:
@@ -479,7 +501,7 @@ class DeviceLattice:
         if not self.has_halo and nsteps >= 4:
             # launch-bound loops: replay a captured two-step graph (buffer
             # ping-pong returns to the same parity), odd remainder eagerly
-            graph = self._pair_graph(kp, key, masks, cm, tm)
+            graph = self._pair_graph(kp, key, masks, cm, tm, lb)
             if graph is not None:
                 # a graph captures kernel arguments, not constant memory:
                 # make the device hold this model's MRT tables again (another
@@ -495,13 +517,13 @@ class DeviceLattice:
         for n in range(nsteps):
             src, dst = self.buf[self.cur], self.buf[1 - self.cur]
             if not self.has_halo:
-                st = lib.lbm_fused_step(self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
-                                        0, nz, self._sp(main))
+                st = lib.lbm_fused_step_bits(self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm,
+                                             tm, lb, 0, nz, self._sp(main))
                 if st:
-                    _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst),
-                              cm, tm, 0, nz, self._sp(main))
+                    _lib.call("lbm_fused_step_bits", self.gref, kp.ref, _lib.ptr(src),
+                              _lib.ptr(dst), cm, tm, lb, 0, nz, self._sp(main))
             else:
-                self._halo_step(kp, src, dst, cm, tm, main)
+                self._halo_step(kp, src, dst, cm, tm, main, lb)
             self.cur = 1 - self.cur
             self.prev_kind = "G"
             self.steps += 1
@@ -512,7 +534,7 @@ class DeviceLattice:
         self.snapshot = None
         self._dst_synced = None
 
-    def _pair_graph(self, kp, key, masks, cm, tm):
+    def _pair_graph(self, kp, key, masks, cm, tm, lb=None):
         """CUDA graph of two fused steps cur -> 1-cur -> cur (P = 1 path).
         Kernel arguments are captured by value, so the graph is keyed by the
         collision key and the buffer parity.  None if capture is unavailable
@@ -533,15 +555,15 @@ class DeviceLattice:
                 with torch.cuda.graph(graph, stream=side):
                     sp = _lib.stream_ptr(torch.cuda.current_stream(self.device))
                     for src, dst in ((a, b), (b, a)):
-                        _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src),
-                                  _lib.ptr(dst), cm, tm, 0, nz, sp)
+                        _lib.call("lbm_fused_step_bits", self.gref, kp.ref, _lib.ptr(src),
+                                  _lib.ptr(dst), cm, tm, lb, 0, nz, sp)
             except Exception:
                 graph = None
             self._graphs[(key, par)] = (graph, masks)   # keeps the mask tensors alive
         self.stream.wait_stream(side)
         return self._graphs[(key, self.cur)][0]
 
-    def _halo_step(self, kp, src, dst, cm, tm, main):
+    def _halo_step(self, kp, src, dst, cm, tm, main, lb=None):
         """One overlapped step: B(n) = boundary planes on the high-priority
         stream, its crossing directions handed to the halo transport (fused
         peer stores or send/recv), I(n) = interior
@@ -559,8 +581,8 @@ class DeviceLattice:
         S["ev_b"].record(sb)
         self.halo.after_boundary(self, dst, sb)
         if nz > 2:
-            _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm, tm,
-                      1, nz - 1, self._sp(main))
+            _lib.call("lbm_fused_step_bits", self.gref, kp.ref, _lib.ptr(src), _lib.ptr(dst), cm,
+                      tm, lb, 1, nz - 1, self._sp(main))
         S["ev_i"].record(main)
         S["pending"] = True
 
@@ -622,10 +644,11 @@ class DeviceLattice:
         c0 = self.cur
         buf = self.buf
         if masks.all_fluid:
-            cm = tm = None
+            cm = tm = lb = None
         else:
             cm = _lib.ptr(masks.cellmask)
             tm = _lib.ptr(masks.typemask) if masks.typed else None
+            lb = masks.linkbits(self)
         sp = self._sp(main)
         done = [0] * (steps + 1)
         mdone = 0
@@ -641,8 +664,9 @@ class DeviceLattice:
             for n in range(1, steps + 1):
                 lim = nz if done[n - 1] == nz else done[n - 1] - 1
                 if lim > done[n]:
-                    _lib.call("lbm_fused_step", self.gref, kp.ref, _lib.ptr(buf[(c0 + n - 1) % 2]),
-                              _lib.ptr(buf[(c0 + n) % 2]), cm, tm, done[n], lim, sp)
+                    _lib.call("lbm_fused_step_bits", self.gref, kp.ref,
+                              _lib.ptr(buf[(c0 + n - 1) % 2]), _lib.ptr(buf[(c0 + n) % 2]), cm, tm,
+                              lb, done[n], lim, sp)
                     done[n] = lim
                     launches += 1
             lim = nz if done[steps - 1] == nz else done[steps - 1] - 1

@@ -26,7 +26,7 @@ def test_library_loads_and_exports_every_header_symbol():
     assert sorted(syms) == sorted(_lib.EXPORTS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.lbm_abi_version() == _lib.ABI_VERSION == 6
+    assert lib.lbm_abi_version() == _lib.ABI_VERSION == 7
 
 
 def test_library_is_sm100a():
