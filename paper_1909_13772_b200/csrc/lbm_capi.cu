@@ -625,7 +625,7 @@ __global__ void k_linkbits_check(KGrid g, const uint32_t* __restrict__ cellmask,
     const int z = blockIdx.z;
     if (x >= g.nx) return;
     const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
-    if (code_from_bits<Q>(g, bits, x, y, z) != cellmask[cell]) atomicMin(mismatch, (int)(cell + 1 < 0x7fffffff ? cell + 1 : 0x7fffffff));
+    if (mask_code_of_nb<Q>(code_from_bits<Q>(g, bits, x, y, z)) != cellmask[cell]) atomicMin(mismatch, (int)(cell + 1 < 0x7fffffff ? cell + 1 : 0x7fffffff));
 }
 
 extern "C" {

@@ -147,39 +147,127 @@ __device__ __forceinline__ uint64_t ldg_bits(const uint64_t* p) {
     return v;
 }
 
+// With the map, a fused kernel works on the NEIGHBOURHOOD word of a cell
+// instead of the mask's code: bits 3 r + b, row r = (dz + 1) * 3 + (dy + 1),
+// b = 0..2 for x - 1 .. x + 1, hold N of the 27 cells around it.  Direction
+// i's link is then bit nb_pos(i) = the bit of x - c_i, and the cell itself
+// (bit 13) replaces LBM_MASK_FLUID: code = N(x) ? 0 : nb | bit 13.  Building
+// it costs one funnel shift + one bit-field insert per row (no per-direction
+// gather); CodeBits<Q, BITS> tells the pull which bit is whose.
+template <int Q>
+__host__ __device__ constexpr int nb_pos(int i) {
+    return 3 * ((1 - Dirs<Q>::cz[i]) * 3 + (1 - Dirs<Q>::cy[i])) + 1 - Dirs<Q>::cx[i];
+}
+constexpr uint32_t kNbCentre = 1u << 13;
+
+template <int Q, bool BITS>
+struct CodeBits {
+    static constexpr uint32_t fluid = BITS ? kNbCentre : LBM_MASK_FLUID;
+    __host__ __device__ static constexpr int link(int i) { return BITS ? nb_pos<Q>(i) : i; }
+};
+
+// bits x .. x + 2 of row word v (lane offset l = x & 31) inserted at 3 r
+template <int R>
+__device__ __forceinline__ uint32_t nb_insert(uint32_t nb, uint64_t v, int l) {
+    const uint32_t s = __funnelshift_r((uint32_t)v, (uint32_t)(v >> 32), l);
+    uint32_t d;
+    asm("bfi.b32 %0, %1, %2, %3, 3;" : "=r"(d) : "r"(s), "r"(nb), "n"(3 * R));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t nb_code(uint32_t nb) {
+    return (nb & kNbCentre) ? 0u : (nb | kNbCentre);
+}
+
+// address of the word holding cell (x - 1 .. x + 1, y, z) of the map
+__device__ __forceinline__ const uint64_t* bits_row(const KGrid& g, const uint64_t* bits, int x,
+                                                    int y, int z) {
+    const int64_t bw = (g.nx + 31) >> 5;
+    return bits + ((int64_t)(z + 1) * (g.ny + 2) + (y + 1)) * bw + (x >> 5);
+}
+
+// L2 prefetch of the map word `ahead` rows (of the plane-major row order)
+// after `w`: the words a block reads first-hand are those of the planes no
+// earlier block touched; the blocks `ahead` rows later read these.
+__device__ __forceinline__ void prefetch_bits(const KGrid& g, const uint64_t* w,
+                                              const uint64_t* end) {
+    const int ahead = g.link_hint >> 1;
+    if (ahead > 0) {
+        const uint64_t* q = w + (int64_t)ahead * ((g.nx + 31) >> 5);
+        if (q < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+    }
+}
+
 template <int Q>
 __device__ __forceinline__ uint32_t code_from_bits(const KGrid& g, const uint64_t* __restrict__ bits,
                                                    int x, int y, int z) {
-    using D = Dirs<Q>;
     const int64_t bw = (g.nx + 31) >> 5;
     const int64_t ps = (int64_t)(g.ny + 2) * bw;
-    const uint64_t* c = bits + ((int64_t)(z + 1) * (g.ny + 2) + (y + 1)) * bw + (x >> 5);
+    const uint64_t* c = bits_row(g, bits, x, y, z);
     const int l = x & 31;
-    uint32_t w[3][3];
+    uint64_t v[9];
     static_for<0, 9>([&](auto R_) {
         constexpr int r = decltype(R_)::value;
-        constexpr int dz = r / 3 - 1, dy = r % 3 - 1;
-        if constexpr (bits_row_used<Q>(dz, dy))
-            w[dz + 1][dy + 1] = (uint32_t)(ldg_bits(c + dz * ps + dy * bw) >> l) & 7u;
-        else
-            w[dz + 1][dy + 1] = 0u;
+        v[r] = ldg_bits(c + (r / 3 - 1) * ps + (r % 3 - 1) * bw);
     });
-    if (w[1][1] & 2u) return 0u;
-    uint32_t code = LBM_MASK_FLUID;
-    static_for<1, Q>([&](auto I_) {
-        constexpr int i = decltype(I_)::value;
-        constexpr int dz = -D::cz[i], dy = -D::cy[i], b = 1 - D::cx[i];
-        code |= ((w[dz + 1][dy + 1] >> b) & 1u) << i;
+    prefetch_bits(g, c + ps + bw, bits + (int64_t)(g.nz + 2) * ps);
+    uint32_t nb = 0u;
+    static_for<0, 9>([&](auto R_) {
+        constexpr int r = decltype(R_)::value;
+        nb = nb_insert<r>(nb, v[r], l);
     });
-    return code;
+    return nb_code(nb);
 }
 
-// the cell code a fused kernel works with: full mask, link bits or none
+// the cell-mask code a neighbourhood word stands for (the map's device check)
+template <int Q>
+__device__ __forceinline__ uint32_t mask_code_of_nb(uint32_t code) {
+    if (!(code & kNbCentre)) return 0u;
+    uint32_t m = LBM_MASK_FLUID;
+    static_for<1, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        m |= ((code >> nb_pos<Q>(i)) & 1u) << i;
+    });
+    return m;
+}
+
+// the cell code a fused kernel works with: full mask, neighbourhood word or none
 template <int Q, bool BITS>
 __device__ __forceinline__ uint32_t cell_code(const KGrid& g, const uint32_t* __restrict__ cellmask,
                                               int x, int y, int z, int64_t cell) {
     if constexpr (BITS) return code_from_bits<Q>(g, reinterpret_cast<const uint64_t*>(cellmask), x, y, z);
     else return cellmask ? __ldg(cellmask + cell) : LBM_MASK_FLUID;
+}
+
+// both cells of a z-pair (za, za + 1) from the 12 words of planes
+// za - 1 .. za + 2 (k_fused_z2)
+template <int Q>
+__device__ __forceinline__ void codes_from_bits_z2(const KGrid& g, const uint64_t* __restrict__ bits,
+                                                   int x, int y, int za, bool two, uint32_t& ca,
+                                                   uint32_t& cb) {
+    const int64_t bw = (g.nx + 31) >> 5;
+    const int64_t ps = (int64_t)(g.ny + 2) * bw;
+    const uint64_t* c = bits_row(g, bits, x, y, za);
+    const int l = x & 31;
+    uint64_t v[12];
+    static_for<0, 12>([&](auto R_) {
+        constexpr int r = decltype(R_)::value;
+        if (r < 9 || two) v[r] = ldg_bits(c + (r / 3 - 1) * ps + (r % 3 - 1) * bw);
+        else v[r] = 0;
+    });
+    {   // the two planes this block reads first-hand
+        const uint64_t* end = bits + (int64_t)(g.nz + 2) * ps;
+        prefetch_bits(g, c + ps + bw, end);
+        prefetch_bits(g, c + 2 * ps + bw, end);
+    }
+    uint32_t na = 0u, nb = 0u;
+    static_for<0, 9>([&](auto R_) {
+        constexpr int r = decltype(R_)::value;
+        na = nb_insert<r>(na, v[r], l);
+        nb = nb_insert<r>(nb, v[r + 3], l);
+    });
+    ca = nb_code(na);
+    cb = two ? nb_code(nb) : 0u;
 }
 
 // (Measured and dropped: L2::128B / L2::256B prefetch-size qualifiers on the
@@ -388,11 +476,13 @@ __device__ __forceinline__ void pull_offsets(const KGrid& g, int x, int y, int z
 // without force accumulation (readouts), 2 moving walls + forces (fused step).
 // Phases 1 + 2 of a pull: source offsets (link substitution as a select)
 // and all Q loads in flight.
-template <int Q, typename Real>
+// BITS: `code` is a neighbourhood word (code_from_bits), see CodeBits.
+template <int Q, typename Real, bool BITS = false>
 __device__ __forceinline__ void pull_load(const KGrid& g, const Real* __restrict__ src, int x,
                                           int y, int z, uint32_t code, bool generic,
                                           Real (&raw)[Q]) {
     using D = Dirs<Q>;
+    using CB = CodeBits<Q, BITS>;
     const int64_t own = lidx(g, z, 0, y, x);
     // link: read the own cell's direction k = opp(i) instead (w_k == w_i, so
     // the fp32 zero-centring offset is the same)
@@ -404,7 +494,7 @@ __device__ __forceinline__ void pull_load(const KGrid& g, const Real* __restrict
             constexpr int i = decltype(I_)::value;
             int d = g.dpull[i];
             // link source = own cell, slot opp(i) (KGrid::dlink)
-            if constexpr (i > 0) d = ((code >> i) & 1u) ? g.dlink[i] : d;
+            if constexpr (i > 0) d = ((code >> CB::link(i)) & 1u) ? g.dlink[i] : d;
             // A bounce-back link of a fluid cell x reads G[x, opp(i)], which
             // the wall cell across the link also pulls.  For directions with
             // c_z = -1 the FIRST of the two reads is either x's link (wall one
@@ -412,7 +502,7 @@ __device__ __forceinline__ void pull_load(const KGrid& g, const Real* __restrict
             // later); that read keeps the line in L2 (evict_last) for the
             // second one instead of leaving it to a whole plane of traffic.
             if constexpr (link_hint<Real>() && D::cz[i] == -1) {
-                if ((g.link_hint & 1) && ((((code >> i) & 1u) != 0u) || !(code & LBM_MASK_FLUID)))
+                if ((g.link_hint & 1) && ((((code >> CB::link(i)) & 1u) != 0u) || !(code & CB::fluid)))
                     raw[i] = ldg_keep(sp + d);
                 else
                     raw[i] = __ldg(sp + d);
@@ -425,7 +515,7 @@ __device__ __forceinline__ void pull_load(const KGrid& g, const Real* __restrict
         pull_offsets<Q, true>(g, x, y, z, own, off);
         static_for<1, Q>([&](auto I_) {
             constexpr int i = decltype(I_)::value;
-            off[i] = ((code >> i) & 1u) ? own + dir_off<Q, D::opp[i]>(g) : off[i];
+            off[i] = ((code >> CB::link(i)) & 1u) ? own + dir_off<Q, D::opp[i]>(g) : off[i];
         });
         static_for<0, Q>([&](auto I_) {
             constexpr int i = decltype(I_)::value;
@@ -441,7 +531,7 @@ __device__ __forceinline__ uint2 type_words(const KGrid& g, const uint32_t* __re
     return __ldg(reinterpret_cast<const uint2*>(typemask) + (((int64_t)z * g.ny + y) * g.nx + x));
 }
 
-template <int Q, typename Real, typename Acc, int MV = 0>
+template <int Q, typename Real, typename Acc, int MV = 0, bool BITS = false>
 __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                                           const Real* __restrict__ src, int x, int y, int z,
                                           uint32_t code, const uint32_t* __restrict__ typemask,
@@ -450,7 +540,7 @@ __device__ __forceinline__ void pull_cell(const KGrid& g, const KParams& p,
                   "fp32 registers only for fp32 storage");
     const uint2 t = type_words(g, typemask, x, y, z, code);
     Real raw[Q];
-    pull_load<Q, Real>(g, src, x, y, z, code, generic, raw);
+    pull_load<Q, Real, BITS>(g, src, x, y, z, code, generic, raw);
     pull_finish<Q, Real, Acc, MV>(g, p, src, x, y, z, lidx(g, z, 0, y, x), code, t, raw, f);
 }
 
@@ -591,8 +681,8 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FO
     if constexpr (!BITS) prefetch_mask(g, cellmask, cell, (int64_t)g.nx * g.ny * g.nz);
     using Acc = AccOf<Real>;
     Acc f[Q];
-    pull_cell<Q, Real, Acc, MOVING ? 2 : 0>(g, p, src, x, y, z, code, typemask, generic, f);
-    if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p, cell);
+    pull_cell<Q, Real, Acc, MOVING ? 2 : 0, BITS>(g, p, src, x, y, z, code, typemask, generic, f);
+    if (code & CodeBits<Q, BITS>::fluid) collide_any<Q, MODEL, FORCE>(f, p, cell);
     Real* dp = opaque(dst + lidx(g, z, 0, y, x));
     static_for<0, Q>([&](auto I_) {
         constexpr int i = decltype(I_)::value;
@@ -657,9 +747,14 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FO
     if (x >= g.nx) return;
     const int64_t plane_cells = (int64_t)g.ny * g.nx;
     const int64_t cell_a = ((int64_t)za * g.ny + y) * g.nx + x;
-    const uint32_t code_a = cell_code<Q, BITS>(g, cellmask, x, y, za, cell_a);
-    const uint32_t code_b = !two ? 0u : cell_code<Q, BITS>(g, cellmask, x, y, za + 1, cell_a + plane_cells);
-    if constexpr (!BITS) {   // both planes of the pair, (link_hint >> 1) pair-rows ahead; a row
+    uint32_t code_a, code_b;
+    if constexpr (BITS) {
+        codes_from_bits_z2<Q>(g, reinterpret_cast<const uint64_t*>(cellmask), x, y, za, two, code_a,
+                              code_b);
+    } else {
+        code_a = cell_code<Q, false>(g, cellmask, x, y, za, cell_a);
+        code_b = !two ? 0u : cell_code<Q, false>(g, cellmask, x, y, za + 1, cell_a + plane_cells);
+        // both planes of the pair, (link_hint >> 1) pair-rows ahead; a row
         // index beyond ny continues in the next plane pair
         const int64_t ncells = (int64_t)g.nx * g.ny * g.nz;
         const int64_t c = (g.link_hint >> 1) > g.ny - 1 - y ? cell_a + plane_cells : cell_a;
@@ -668,14 +763,14 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FO
     }
     using Acc = AccOf<Real>;
     Real ra[Q], rb[Q];
-    pull_load<Q, Real>(g, src, x, y, za, code_a, edge_xy || plane_wraps(g, za), ra);
-    if (two) pull_load<Q, Real>(g, src, x, y, za + 1, code_b, edge_xy || plane_wraps(g, za + 1), rb);
+    pull_load<Q, Real, BITS>(g, src, x, y, za, code_a, edge_xy || plane_wraps(g, za), ra);
+    if (two) pull_load<Q, Real, BITS>(g, src, x, y, za + 1, code_b, edge_xy || plane_wraps(g, za + 1), rb);
     auto finish = [&](int z, int64_t cell, uint32_t code, const Real (&raw)[Q]) {
         Acc f[Q];
         const uint2 t = TYPED ? type_words(g, typemask, x, y, z, code) : make_uint2(0u, 0u);
         pull_finish<Q, Real, Acc, 0, TYPED>(g, p, src, x, y, z, lidx(g, z, 0, y, x), code, t, raw,
                                             f);
-        if (code & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p, cell);
+        if (code & CodeBits<Q, BITS>::fluid) collide_any<Q, MODEL, FORCE>(f, p, cell);
         Real* dp = opaque(dst + lidx(g, z, 0, y, x));
         static_for<0, Q>([&](auto I_) {
             constexpr int i = decltype(I_)::value;

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import gc
+import os
 
 import numpy as np
 import torch
@@ -139,6 +140,13 @@ class RankBox:
                                          ox:ox + v.shape[2]], 0, 3)
 
 
+def linkbits_enabled() -> bool:
+    """The link-bit map is opt-in (LBM_B200_LINKBITS=1): measured on B200 it
+    moves 3.75 B/cell less but runs config 4 fp32 3.6 % and fp64 1.9 % slower
+    than the prefetched cell mask (profiles/ab_variants_r2.md §4)."""
+    return os.environ.get("LBM_B200_LINKBITS", "0") == "1"
+
+
 class Masks:
     """Device cell mask + link-type mask for one (box, stencil, flags) state."""
 
@@ -158,7 +166,7 @@ class Masks:
         Pressure) links, moving walls, or a mask the bits cannot express
         (flags edited after freeze()).  Built once per mask, checked on the
         device on every cell (one sync, at setup)."""
-        if self.all_fluid or self.typed or not self.bits_ok:
+        if self.all_fluid or self.typed or not self.bits_ok or not linkbits_enabled():
             return None
         if self._linkbits is None:
             n = int(_lib.load().lbm_linkbits_words(lat.gref))

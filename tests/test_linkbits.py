@@ -34,6 +34,13 @@ def api():
     return cases.b200_api()
 
 
+@pytest.fixture(autouse=True)
+def _linkbits_on(monkeypatch):
+    """The map is opt-in (device.linkbits_enabled); tests that compare with
+    the cell-mask kernel switch it off again with LBM_B200_LINKBITS=0."""
+    monkeypatch.setenv("LBM_B200_LINKBITS", "1")
+
+
 def _ctx():
     import paper_1909_13772_b200 as P
     return P.Context()
