@@ -155,10 +155,10 @@ _VECTORS = ("position", "orientation", "linear_velocity", "angular_velocity",
 
 
 def pack_body(buf, body):
-    for v in (body.uid, 0):
-        buf.pack_int(v)
-    for v in (body.shape.radius, body.mass):
-        buf.pack_float(v)
+    buf.pack_int(body.uid)
+    buf.pack_int(0)                       # shape kind: sphere
+    buf.pack_float(body.shape.radius)
+    buf.pack_float(body.mass)
     for name in _VECTORS:
         buf.pack_floats(getattr(body, name))
     buf.pack_bool(bool(body._kicked))
@@ -227,11 +227,16 @@ def handler_of(forest, key):
     raise ValidationError(f"slot {key!r} is not a body storage")
 
 
+def _storages(forest, key):
+    """(block, its BodyStorage) for every block of this rank."""
+    return [(blk, blk.data[key]) for blk in forest.local_blocks()]
+
+
 def _stored(forest, key, label=None):
-    for block in forest.local_blocks():
-        for _, body in sorted(block.data[key].bodies.items()):
+    for blk, store in _storages(forest, key):
+        for _, body in sorted(store.bodies.items()):
             if label is None or body.classification == label:
-                yield block, body
+                yield blk, body
 
 
 def _inside(box, p):
@@ -249,8 +254,7 @@ def add_sphere(forest, position, radius, *, key="bodies", mass=None, density=Non
     shape = Sphere(radius)
     if density is not None:
         mass = _positive(density, "density") * 4.0 / 3.0 * math.pi * shape.radius ** 3
-    top = max((uid for block in forest.local_blocks() for uid in block.data[key].bodies),
-              default=-1)
+    top = max((uid for _, store in _storages(forest, key) for uid in store.bodies), default=-1)
     uid = int(forest.ctx.all_reduce((top,), "max")[0]) + 1
     home = next((b for b in forest.local_blocks() if _inside(forest.block_aabb(b.id), position)),
                 None)
@@ -332,8 +336,8 @@ def sync_bodies(forest, *, key="bodies"):
     lo, hi = np.asarray(forest.domain[:3]), np.asarray(forest.domain[3:])
     extent = hi - lo
     reach_extra = handler_of(forest, key).contact_threshold
-    for block in forest.local_blocks():
-        block.data[key].clear_ghosts()
+    for _, store in _storages(forest, key):
+        store.clear_ghosts()
 
     def adopt(item):
         bid, body = item
@@ -343,19 +347,19 @@ def sync_bodies(forest, *, key="bodies"):
         forest.blocks[bid].data[key].add(body)
 
     movers = _Mailbox(ctx, adopt)
-    for block in forest.local_blocks():
-        own_box = forest.block_aabb(block.id)
-        for body in block.data[key].local():
+    for blk, store in _storages(forest, key):
+        own_box = forest.block_aabb(blk.id)
+        for body in store.local():
             if _inside(own_box, body.position):
                 continue
             dest = next(((bid, shift, rank) for bid, shift, rank, box in
-                         _neighbour_images(forest, block, extent)
+                         _neighbour_images(forest, blk, extent)
                          if _inside(box, body.position)), None)
             if dest is None:
                 raise SyncError(f"body {body.uid} moved farther than one block in one step "
                                 "(or left the domain)")
             bid, shift, rank = dest
-            block.data[key].remove(body.uid)
+            store.remove(body.uid)
             if any(shift):
                 body.position = body.position - np.asarray(shift, dtype=np.float64) * extent
             movers.post(rank, (bid, body))
@@ -372,14 +376,14 @@ def sync_bodies(forest, *, key="bodies"):
         storage.add(ghost)
 
     ghosts = _Mailbox(ctx, place)
-    for block in forest.local_blocks():
-        images = _neighbour_images(forest, block, extent)
-        for body in block.data[key].local():
+    for blk, store in _storages(forest, key):
+        images = _neighbour_images(forest, blk, extent)
+        for body in store.local():
             reach = body.bounding_radius + reach_extra
             for bid, shift, rank, box in images:
                 if _gap2(box, body.position) > reach * reach:
                     continue
-                if bid == block.id:
+                if bid == blk.id:
                     raise SyncError(f"body {body.uid} overlaps its own periodic image; the "
                                     "domain is too small for its size")
                 offset = np.asarray(shift, dtype=np.float64) * extent if any(shift) else None
