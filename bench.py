@@ -521,7 +521,8 @@ def run_e2e(args, cfg, ctx, dtype, P, forest, pdf, handling, model, force, dims)
             "breakdown": {k: round(v, 2) for k, v in phases.items()},
             "timed": "P.run_arrays: pinned host rho/u -> H2D -> equilibrium -> K sweeps -> "
                      "moments -> D2H into pinned host rho/u, "
-                     + ("as a wavefront over 32-plane chunks (copies overlap the sweeps), "
+                     + ("as a wavefront over z-plane chunks (4, 4, 8, 16, then 32 planes; 4-plane "
+                        "tail steps; copies overlap the sweeps), "
                         if pipelined else "as the call sequence (periodic z or several ranks), ")
                      + "wall clock, max over ranks, after one untimed pass of the same job; "
                        "breakdown = the unpipelined call sequence replayed untimed"}

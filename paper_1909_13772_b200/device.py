@@ -147,6 +147,81 @@ def linkbits_enabled() -> bool:
     return os.environ.get("LBM_B200_LINKBITS", "0") == "1"
 
 
+def job_schedule(nz, steps, chunk=None):
+    """Upload chunks and wavefront frontiers of DeviceLattice.run_job.
+
+    `chunk` = (planes, ramp, tail): chunks of `planes` z-planes, preceded by
+    the smaller `ramp` chunks (the first sweeps start after a short upload
+    instead of a whole chunk); once every plane is filled the frontier keeps
+    advancing `tail` planes at a time past nz, so the last steps, moments
+    and downloads also move in small pieces (0: the last chunk's steps run
+    to the end in one launch each).  An int is (planes, (), 0); None the
+    defaults (32, (4, 4, 8, 16), 4), or LBM_B200_JOB_CHUNK / _RAMP / _TAIL.
+    Returns ([(z0, z1)], [frontier]); frontiers past nz are tail steps."""
+    if chunk is None:
+        planes = int(os.environ.get("LBM_B200_JOB_CHUNK", "32"))
+        ramp = tuple(int(v) for v in os.environ.get("LBM_B200_JOB_RAMP", "4,4,8,16").split(",")
+                     if v.strip())
+        tail = int(os.environ.get("LBM_B200_JOB_TAIL", "4"))
+    elif isinstance(chunk, int):
+        planes, ramp, tail = chunk, (), 0
+    else:
+        planes, ramp, tail = chunk
+    planes = max(1, int(planes))
+    bounds, z = [], 0
+    for size in tuple(ramp) + (planes,) * nz:
+        if z >= nz:
+            break
+        bounds.append((z, min(z + max(1, int(size)), nz)))
+        z = bounds[-1][1]
+    fronts = [z1 for _, z1 in bounds]
+    if tail > 0:
+        f = nz
+        while f - steps < nz:
+            f += int(tail)
+            fronts.append(f)
+    return bounds, fronts
+
+
+def job_plan(nz, steps, chunk=None):
+    """The ordered launches of DeviceLattice.run_job: ("fill", chunk index,
+    z0, z1), ("step", n, z0, z1) - sweep n (G_{n-1} -> G_n) over planes
+    [z0, z1) - and ("moments", z0, z1) - rho / u of R_K = S(G_{K-1}).
+
+    G_n lives in buffer n % 2 (relative), so step n at plane p reads G_{n-1}
+    on p - 1 .. p + 1 and overwrites G_{n-2} on p, which step n - 1 still
+    needs up to p + 1: step n may finish the planes below done[n-1] - 1 (all
+    of them once step n - 1 is complete).  The moments read G_{K-1} like a
+    step K would.  Past the last chunk, tail frontiers cap step n at
+    front - n.  tests/test_abi_host.py checks these rules for many
+    schedules; tests/test_pipeline.py that the job is bitwise the call
+    sequence on the GPU."""
+    bounds, fronts = job_schedule(nz, steps, chunk)
+    capped = fronts[-1] > nz
+    done = [0] * (steps + 1)
+    mdone, ci, plan = 0, 0, []
+
+    def frontier(prev, n, front):
+        lim = nz if prev == nz else prev - 1
+        return min(lim, front - n) if capped and front - n < nz else lim
+
+    for front in fronts:
+        if ci < len(bounds) and bounds[ci][1] == front:
+            plan.append(("fill", ci) + bounds[ci])
+            done[0] = bounds[ci][1]
+            ci += 1
+        for n in range(1, steps + 1):
+            lim = frontier(done[n - 1], n, front)
+            if lim > done[n]:
+                plan.append(("step", n, done[n], lim))
+                done[n] = lim
+        lim = frontier(done[steps - 1], steps, front)
+        if lim > mdone:
+            plan.append(("moments", mdone, lim))
+            mdone = lim
+    return plan
+
+
 class Masks:
     """Device cell mask + link-type mask for one (box, stencil, flags) state."""
 
@@ -605,15 +680,10 @@ class DeviceLattice:
         """fill_equilibrium_arrays -> `steps` fused sweeps -> moments of R_K,
         as a wavefront over chunks of z-planes so the PCIe copies overlap the
         sweeps.  Same kernels and arithmetic as the call sequence, in another
-        order; bitwise identical results and end state.
-
-        G_n lives in buf[(c0 + n) % 2].  Step n of plane p reads G_{n-1} on
-        planes p-1..p+1 and overwrites G_{n-2} on plane p, which step n-1
-        still needs up to plane p+1: with done[n] = planes [0, done[n]) of
-        G_n finished, step n may advance to done[n-1] - 1 (to nz once step
-        n-1 is complete); the moments of R_K = S(G_{K-1}) follow step K-1
-        the same way.  Uncovered z ghost planes keep their fill values in
-        both buffers (fill writes the other buffer's shell)."""
+        order (job_plan: the dependency rules, ramp and tail); bitwise
+        identical results and end state.  G_n lives in buf[(c0 + n) % 2].
+        Uncovered z ghost planes keep their fill values in both buffers (fill
+        writes the other buffer's shell).  `chunk`: see job_schedule."""
         b = self.box
         nz = b.nz
         self.join_streams()
@@ -636,11 +706,7 @@ class DeviceLattice:
         up.wait_stream(main)
         main.wait_stream(dn)
         st["bad"].zero_()
-        if chunk is None:
-            import os
-            chunk = int(os.environ.get("LBM_B200_JOB_CHUNK", "32"))
-        chunk = max(1, min(int(chunk), nz))
-        bounds = [(z, min(z + chunk, nz)) for z in range(0, nz, chunk)]
+        bounds, _ = job_schedule(nz, steps, chunk)
         evs = []
         with torch.cuda.stream(up):
             for z0, z1 in bounds:
@@ -658,38 +724,34 @@ class DeviceLattice:
             tm = _lib.ptr(masks.typemask) if masks.typed else None
             lb = masks.linkbits(self)
         sp = self._sp(main)
-        done = [0] * (steps + 1)
-        mdone = 0
         launches = 0
-        for (z0, z1), ev in zip(bounds, evs):
-            main.wait_event(ev)
-            # equilibrium + G_0 = C(R_0) of the chunk in one pass (the other
-            # buffer gets the ghost shell)
-            _lib.call("lbm_fill_collide_planes", self.gref, kp.ref, _lib.ptr(st["rho"]),
-                      _lib.ptr(st["u"]), z0, z1, _lib.ptr(buf[c0]), _lib.ptr(buf[1 - c0]),
-                      _lib.ptr(masks.cellmask), sp)
-            done[0] = z1
-            for n in range(1, steps + 1):
-                lim = nz if done[n - 1] == nz else done[n - 1] - 1
-                if lim > done[n]:
-                    _lib.call("lbm_fused_step_bits", self.gref, kp.ref,
-                              _lib.ptr(buf[(c0 + n - 1) % 2]), _lib.ptr(buf[(c0 + n) % 2]), cm, tm,
-                              lb, done[n], lim, sp)
-                    done[n] = lim
-                    launches += 1
-            lim = nz if done[steps - 1] == nz else done[steps - 1] - 1
-            if lim > mdone:
+        for act in job_plan(nz, steps, chunk):
+            if act[0] == "fill":
+                _, ci, z0, z1 = act
+                main.wait_event(evs[ci])
+                # equilibrium + G_0 = C(R_0) of the chunk in one pass (the
+                # other buffer gets the ghost shell)
+                _lib.call("lbm_fill_collide_planes", self.gref, kp.ref, _lib.ptr(st["rho"]),
+                          _lib.ptr(st["u"]), z0, z1, _lib.ptr(buf[c0]), _lib.ptr(buf[1 - c0]),
+                          _lib.ptr(masks.cellmask), sp)
+            elif act[0] == "step":
+                _, n, z0, z1 = act
+                _lib.call("lbm_fused_step_bits", self.gref, kp.ref,
+                          _lib.ptr(buf[(c0 + n - 1) % 2]), _lib.ptr(buf[(c0 + n) % 2]), cm, tm,
+                          lb, z0, z1, sp)
+                launches += 1
+            else:
+                _, z0, z1 = act
                 _lib.call("lbm_moments_planes", self.gref, kp_mom.ref,
                           _lib.ptr(buf[(c0 + steps - 1) % 2]), _lib.ptr(masks.cellmask),
-                          _lib.ptr(masks.typemask), 1, mdone, lim, _lib.ptr(st["rho_o"]),
+                          _lib.ptr(masks.typemask), 1, z0, z1, _lib.ptr(st["rho_o"]),
                           _lib.ptr(st["u_o"]), _lib.ptr(st["bad"]), sp)
                 evm = torch.cuda.Event()
                 evm.record(main)
                 dn.wait_event(evm)
                 with torch.cuda.stream(dn):
-                    out[0][mdone:lim].copy_(st["rho_o"][mdone:lim], non_blocking=True)
-                    out[1][mdone:lim].copy_(st["u_o"][mdone:lim], non_blocking=True)
-                mdone = lim
+                    out[0][z0:z1].copy_(st["rho_o"][z0:z1], non_blocking=True)
+                    out[1][z0:z1].copy_(st["u_o"][z0:z1], non_blocking=True)
         dn.synchronize()
         # end state: exactly what the call sequence leaves
         self.cur = (c0 + steps) % 2

@@ -253,3 +253,48 @@ def test_host_exchange_and_gather_single_rank():
             assert v[zz + 1, yy + 1, xx + 1] == gx + 10 * gy + 100 * gz
     full = P.gather_slice(forest, "s", (0, 0, 0), N)
     assert full.shape == (2, 3, 8, 1) and full[1, 2, 7, 0] == 7 + 20 + 100
+
+
+# ------------------------------------------------ run_arrays wavefront plan
+@pytest.mark.parametrize("nz,steps,chunk", [
+    (512, 20, None), (512, 100, None), (40, 7, 8), (40, 30, 6), (44, 9, 44), (44, 4, 1),
+    (41, 6, 3), (10, 30, (4, (1, 2), 3)), (33, 5, (7, (1,), 1)), (5, 3, (2, (), 9)),
+    (1, 4, None), (2, 1, None), (64, 1, (32, (4, 4, 8, 16), 4)),
+])
+def test_job_plan_respects_the_sweep_dependencies(nz, steps, chunk):
+    """DeviceLattice.run_job's launch order (device.job_plan), simulated on
+    the host: each plane of G_n is written once, only after G_{n-1} holds its
+    neighbours (p - 1 .. p + 1; z ghosts are fixed) and before nothing still
+    needs the G_{n-2} it overwrites; the moments read finished G_{K-1}
+    planes; every plane is filled, swept K times and read out once."""
+    from paper_1909_13772_b200.device import job_plan, job_schedule
+    plan = job_plan(nz, steps, chunk)
+    bounds, _ = job_schedule(nz, steps, chunk)
+    assert [a[2:] for a in plan if a[0] == "fill"] == bounds
+    ver = np.full(nz, -1)                 # ver[p]: newest G_n written on plane p
+    reads = {}                            # (n, p): readers of G_n on p still to come
+    moments = np.zeros(nz, dtype=bool)
+    for act in plan:
+        if act[0] == "fill":
+            _, _, z0, z1 = act
+            assert (ver[z0:z1] == -1).all()
+            ver[z0:z1] = 0
+            continue
+        if act[0] == "step":
+            _, n, z0, z1 = act
+        else:
+            (_, z0, z1), n = act, steps
+        for p in range(z0, z1):
+            for q in (p - 1, p, p + 1):
+                if 0 <= q < nz:
+                    # G_{n-1} on q is there and not yet overwritten by G_{n+1}
+                    assert ver[q] in (n - 1, n), (act, q, ver[q])
+            if act[0] == "step":
+                assert ver[p] == n - 1
+                # overwriting G_{n-2} on p: step n-1 is past p + 1
+                assert p + 1 >= nz or ver[p + 1] >= n - 1
+                ver[p] = n
+            else:
+                assert not moments[p]
+                moments[p] = True
+    assert (ver == steps).all() and moments.all()
