@@ -27,13 +27,6 @@ inline dim3 cell_block(int nx) {
     return dim3(bx, 1, 1);
 }
 
-// LBM_B200_ZN=2..4: the k_fused_zn A/B variant (0 = off, the default)
-inline int use_zn() {
-    const char* e = getenv("LBM_B200_ZN");
-    const int v = e ? atoi(e) : 0;
-    return v >= 2 && v <= 4 ? v : 0;
-}
-
 inline bool use_z2() {
     const char* e = getenv("LBM_B200_Z2");
     return !(e && e[0] == '0');
@@ -215,7 +208,7 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
     // corrections' register demand would make it spill, so typed launches
     // keep k_fused).  LBM_B200_Z2=0 selects k_fused (A/B runs).
     if constexpr (std::is_same_v<LBM_REAL, float> && Q == 19 && (MODEL == 0 || MODEL == 1)) {
-        if (!p.mv_link && !peer && !tmk && use_z2() && !use_zn()) {
+        if (!p.mv_link && !peer && !tmk && use_z2()) {
             dim3 grid2(grid.x, grid.y, (z1 - z0 + 1) / 2);
             if (bits)
                 k_fused_z2<Q, LBM_REAL, MODEL, FORCE, false, true><<<grid2, b, 0, s>>>(
@@ -224,23 +217,6 @@ cudaError_t fused_t(const KGrid& g, const KParams& p, const void* src, void* dst
                 k_fused_z2<Q, LBM_REAL, MODEL, FORCE, false><<<grid2, b, 0, s>>>(
                     g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, tmk, z0, z1);
             return cudaGetLastError();
-        }
-    }
-    // A/B variant: ZN cells per thread along z (k_fused_zn), D3Q19 SRT / TRT
-    // NoSlip-only sweeps of either storage type
-    if constexpr (Q == 19 && (MODEL == 0 || MODEL == 1)) {
-        const int zn = use_zn();
-        if (zn >= 2 && !p.mv_link && !peer && !tmk && !bits) {
-            auto launch = [&](auto Nc) {
-                constexpr int N = decltype(Nc)::value;
-                dim3 gridn(grid.x, grid.y, (z1 - z0 + N - 1) / N);
-                k_fused_zn<Q, LBM_REAL, MODEL, FORCE, N><<<gridn, b, 0, s>>>(
-                    g, p, (const LBM_REAL*)src, (LBM_REAL*)dst, cm, z0, z1);
-                return cudaGetLastError();
-            };
-            if (zn == 2) return launch(std::integral_constant<int, 2>{});
-            if (zn == 3) return launch(std::integral_constant<int, 3>{});
-            return launch(std::integral_constant<int, 4>{});
         }
     }
     if constexpr (bits_variant<Q, MODEL, FORCE>()) {

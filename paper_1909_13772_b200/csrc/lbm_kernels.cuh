@@ -781,71 +781,6 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_z2_minb<Q, Real, MODEL, FO
     if (two) finish(za + 1, cell_a + plane_cells, code_b, rb);
 }
 
-// ZN cells per thread stacked in z (A/B variant of k_fused / k_fused_z2:
-// LBM_B200_ZN=n, n = 2..4, NoSlip-only masks): all ZN cells' pulls are in
-// flight before the first is finished.  Same arithmetic per cell.
-template <typename Real, int ZN>
-constexpr int fused_zn_minb() {
-#ifdef LBM_FUSED_ZN_MINB
-    return LBM_FUSED_ZN_MINB;
-#else
-    return std::is_same_v<Real, double> ? (ZN == 2 ? 4 : 3) : (ZN == 2 ? 6 : ZN == 3 ? 5 : 4);
-#endif
-}
-
-template <int Q, typename Real, int MODEL, int FORCE, int ZN>
-__global__ void __launch_bounds__(LBM_FUSED_BX, fused_zn_minb<Real, ZN>())
-    k_fused_zn(KGrid g, KParams p, const Real* __restrict__ src, Real* __restrict__ dst,
-               const uint32_t* __restrict__ cellmask, int z0, int z1) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y;
-    const int za = z0 + ZN * blockIdx.z;
-    const int nb = z1 - za < ZN ? z1 - za : ZN;        // block-uniform
-    const int xw0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-    const bool edge_xy = (g.wrap_x && (xw0 == 0 || xw0 + 32 >= g.nx)) ||
-                         (g.wrap_y && (y == 0 || y == g.ny - 1));
-    if (x >= g.nx) return;
-    const int64_t plane_cells = (int64_t)g.ny * g.nx;
-    const int64_t cell_a = ((int64_t)za * g.ny + y) * g.nx + x;
-    uint32_t code[ZN];
-    static_for<0, ZN>([&](auto K_) {
-        constexpr int k = decltype(K_)::value;
-        code[k] = k >= nb ? 0u : cellmask ? __ldg(cellmask + cell_a + k * plane_cells) : LBM_MASK_FLUID;
-    });
-    {   // every plane of the group, (link_hint >> 1) rows ahead; a row index
-        // beyond ny continues in the next plane group
-        const int64_t ncells = (int64_t)g.nx * g.ny * g.nz;
-        const int64_t c = (g.link_hint >> 1) > g.ny - 1 - y ? cell_a + (ZN - 1) * plane_cells : cell_a;
-        static_for<0, ZN>([&](auto K_) {
-            constexpr int k = decltype(K_)::value;
-            prefetch_mask(g, cellmask, c + k * plane_cells, ncells);
-        });
-    }
-    using Acc = AccOf<Real>;
-    Real raw[ZN][Q];
-    static_for<0, ZN>([&](auto K_) {
-        constexpr int k = decltype(K_)::value;
-        if (k < nb)
-            pull_load<Q, Real>(g, src, x, y, za + k, code[k], edge_xy || plane_wraps(g, za + k),
-                               raw[k]);
-    });
-    static_for<0, ZN>([&](auto K_) {
-        constexpr int k = decltype(K_)::value;
-        if (k < nb) {
-            const int z = za + k;
-            Acc f[Q];
-            pull_finish<Q, Real, Acc, 0, false>(g, p, src, x, y, z, lidx(g, z, 0, y, x), code[k],
-                                                make_uint2(0u, 0u), raw[k], f);
-            if (code[k] & LBM_MASK_FLUID) collide_any<Q, MODEL, FORCE>(f, p, cell_a + k * plane_cells);
-            Real* dp = opaque(dst + lidx(g, z, 0, y, x));
-            static_for<0, Q>([&](auto I_) {
-                constexpr int i = decltype(I_)::value;
-                store_any<Q, i>(dp + g.dslot[i], f[i]);
-            });
-        }
-    });
-}
-
 // G_0 = C(R_0): collide fluid interior cells in place.
 template <int Q, typename Real, int MODEL, int FORCE>
 __global__ void __launch_bounds__(128) k_collide_only(KGrid g, KParams p, Real* __restrict__ pdf,
