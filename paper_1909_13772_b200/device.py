@@ -156,13 +156,16 @@ def job_schedule(nz, steps, chunk=None):
     advancing `tail` planes at a time past nz, so the last steps, moments
     and downloads also move in small pieces (0: the last chunk's steps run
     to the end in one launch each).  An int is (planes, (), 0); None the
-    defaults (32, (4, 4, 8, 16), 4), or LBM_B200_JOB_CHUNK / _RAMP / _TAIL.
+    defaults (32, (4, 4, 8, 16), max(4, ceil(steps / 2))), or
+    LBM_B200_JOB_CHUNK / _RAMP / _TAIL.
     Returns ([(z0, z1)], [frontier]); frontiers past nz are tail steps."""
     if chunk is None:
         planes = int(os.environ.get("LBM_B200_JOB_CHUNK", "32"))
         ramp = tuple(int(v) for v in os.environ.get("LBM_B200_JOB_RAMP", "4,4,8,16").split(",")
                      if v.strip())
-        tail = int(os.environ.get("LBM_B200_JOB_TAIL", "4"))
+        # two or three tail frontiers (each issues up to `steps` launches;
+        # measured at 512^3 K = 20 and 128^3 K = 100, profiles/r2/e2e_tail.log)
+        tail = int(os.environ.get("LBM_B200_JOB_TAIL", str(max(4, -(-steps // 2)))))
     elif isinstance(chunk, int):
         planes, ramp, tail = chunk, (), 0
     else:

@@ -77,3 +77,30 @@ for rep in range(3):
         print(f"{name:12s} K={K}: job {ms:8.2f} ms  last launch enqueued at {enq:8.2f} ms  "
               f"({n} calls)  -> {dims[0]*dims[1]*dims[2]*K/ms/1e3:8.1f} MLUPS")
 print(f"sweep (graph) ms/step after: {sweeps(10):.3f}")
+
+
+def ranges(width, reps=5):
+    """One sweep as nz / width plane-range launches (no graph), ms per sweep."""
+    from paper_1909_13772_b200.lbm import sweep as S
+    lat, kp, key, masks = S._prepare(pdf, model, force, handling)
+    nz = lat.box.nz
+    src, dst = lat.buf[lat.cur], lat.buf[1 - lat.cur]
+    sp = lat._sp()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for r in range(reps):
+        a, b = (src, dst) if r % 2 == 0 else (dst, src)
+        for z0 in range(0, nz, width):
+            orig("lbm_fused_step_bits", lat.gref, kp.ref, _lib.ptr(a), _lib.ptr(b),
+                 _lib.ptr(masks.cellmask), None, None, z0, min(nz, z0 + width), sp)
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+for w in (512, 128, 64, 32, 16, 8, 4):
+    ms = ranges(w)
+    print(f"one sweep as {512 // w:3d} launches of {w:3d} planes: {ms:.3f} ms "
+          f"(+{(ms - 0) * 1e3 / (512 // w):.1f} us per launch incl. work)")
