@@ -87,7 +87,7 @@
 extern "C" {
 #endif
 
-#define LBM_B200_ABI_VERSION 7
+#define LBM_B200_ABI_VERSION 8
 
 /* status codes */
 #define LBM_OK 0
@@ -338,6 +338,22 @@ int lbm_moments_planes(const lbm_grid_t* g, const lbm_params_t* p,
                        const uint32_t* typemask, int stream_form, int z0,
                        int z1, double* rho, double* u, int* bad_count,
                        void* stream);
+
+/* lbm_fused_step over [z0, z1) that also writes rho / u of the state it
+ * pulls - R = S(src), bitwise lbm_moments_planes(p_moments, src,
+ * stream_form = 1) - into the whole-box rho (nz,ny,nx) / u (nz,ny,nx,3)
+ * (ABI 8).  One pass where the sweep's own rho / u are the readout's (fp64
+ * D3Q19 SRT / TRT, unforced or Guo with p_moments' shift; no moving walls):
+ * the last sweep of a job hands back its moments without a second pass
+ * over the field (reference: stream_collide then macroscopic_fields,
+ * sweep.py:93-183).  Elsewhere the readout and the sweep run as two
+ * launches (cellmask and typemask required then). */
+int lbm_fused_step_moments(const lbm_grid_t* g, const lbm_params_t* p,
+                           const lbm_params_t* p_moments, const void* src,
+                           void* dst, const uint32_t* cellmask,
+                           const uint32_t* typemask, int z_begin, int z_end,
+                           double* rho, double* u, int* bad_count,
+                           void* stream);
 
 /* Flag validation + link masks from ghost-inclusive flags (Z, Y, X) uint32.
  * bits: [0]=Fluid [1]=NoSlip [2]=UBB [3]=Pressure [4]=Solid registry masks.

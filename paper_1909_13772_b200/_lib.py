@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lbm_b200.so"
 
 LBM_OK, LBM_EINVAL, LBM_ECUDA, LBM_ENUMERIC, LBM_EFLAGS = 0, -1, -2, -3, -4
 ZFACE_GHOST, ZFACE_HALO, ZFACE_WRAP = 0, 1, 2
-ABI_VERSION = 7
+ABI_VERSION = 8
 SRT, TRT, MRT, SRT_FIELD = 0, 1, 2, 3
 MASK_FLUID = 0x1
 MASK_UBB = 0x80000000
@@ -34,7 +34,7 @@ EXPORTS = (
     "lbm_bind_params", "lbm_slot_collide", "lbm_slot_stream_pull", "lbm_refresh_fluid_mask",
     "lbm_map_spheres", "lbm_copy_shell", "lbm_slot_apply_links",
     "lbm_fill_equilibrium_planes", "lbm_collide_only_planes", "lbm_moments_planes",
-    "lbm_fill_collide_planes", "lbm_can_flush_remote_writes",
+    "lbm_fill_collide_planes", "lbm_can_flush_remote_writes", "lbm_fused_step_moments",
     "lbm_fused_step_bits", "lbm_linkbits_words", "lbm_build_linkbits",
 )
 
@@ -123,6 +123,7 @@ def load(path: Path | None = None):
         "lbm_fill_equilibrium_planes": ([G, P, P, I, I, P, P, P], I),
         "lbm_collide_only_planes": ([G, PR, P, P, I, I, P], I),
         "lbm_moments_planes": ([G, PR, P, P, P, I, I, I, P, P, P, P], I),
+        "lbm_fused_step_moments": ([G, PR, PR, P, P, P, P, I, I, P, P, P, P], I),
         "lbm_fill_collide_planes": ([G, PR, P, P, I, I, P, P, P, P], I),
         "lbm_can_flush_remote_writes": ([], I),
         "lbm_fused_step_bits": ([G, PR, P, P, P, P, P, I, I, P], I),

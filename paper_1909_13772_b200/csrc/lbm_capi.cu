@@ -926,6 +926,45 @@ static int moments_range(const lbm_grid_t* g, const lbm_params_t* p, const void*
     return cuda_status(e, who);
 }
 
+int lbm_fused_step_moments(const lbm_grid_t* g, const lbm_params_t* p, const lbm_params_t* p_moments,
+                           const void* src, void* dst, const uint32_t* cellmask,
+                           const uint32_t* typemask, int z_begin, int z_end, double* rho, double* u,
+                           int* bad_count, void* stream) {
+    KGrid k;
+    KParams kp;
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = check_grid(g, &k);
+    if (st != LBM_OK) return st;
+    if ((st = check_params(p, g->q, &kp, s, g->real_bytes)) != LBM_OK) return st;
+    if (!p_moments || !src || !dst || !rho || !u || !bad_count) return fail(LBM_EINVAL, "NULL buffer");
+    if (src == dst) return fail(LBM_EINVAL, "fused step needs two fields (src != dst)");
+    if (z_begin < 0 || z_end > g->nz || z_begin > z_end)
+        return fail(LBM_EINVAL, "plane range [%d, %d) outside 0..%d", z_begin, z_end, g->nz);
+    // one pass where the sweep's own rho / u ARE the readout's: the readout
+    // is Guo-shifted exactly when the sweep is, by the same shift
+    auto guo = [](const lbm_params_t* q) {
+        return q->force_mode == LBM_FORCE_GUO || q->force_mode == LBM_FORCE_GUO_X;
+    };
+    const bool same = guo(p) == guo(p_moments) && (p->force_mode == LBM_FORCE_NONE || guo(p)) &&
+                      (!guo(p) || (p->shift_fx == p_moments->shift_fx &&
+                                   p->shift_fy == p_moments->shift_fy &&
+                                   p->shift_fz == p_moments->shift_fz));
+    if (same && g->real_bytes == 8) {
+        cudaError_t e = unit_f64::fused_mom(g->q, p->model, p->force_mode, k, kp, src, dst, cellmask,
+                                            typemask, z_begin, z_end, rho, u, bad_count, s);
+        if (e != cudaErrorNotSupported) return cuda_status(e, "lbm_fused_step_moments");
+    }
+    // elsewhere: the readout of src, then the sweep (stream order)
+    if (cellmask && typemask) {
+        st = moments_range(g, p_moments, src, cellmask, typemask, 1, z_begin, z_end, rho, u,
+                           bad_count, stream, "lbm_fused_step_moments");
+        if (st != LBM_OK) return st;
+    } else {
+        return fail(LBM_EINVAL, "this lattice needs cellmask and typemask for the readout");
+    }
+    return lbm_fused_step(g, p, src, dst, cellmask, typemask, z_begin, z_end, stream);
+}
+
 int lbm_moments(const lbm_grid_t* g, const lbm_params_t* p, const void* src,
                 const uint32_t* cellmask, const uint32_t* typemask, int stream_form, double* rho,
                 double* u, int* bad_count, void* stream) {

@@ -175,8 +175,11 @@ __device__ __forceinline__ double guo_F(double ux, double uy, double uz, double 
 // MODEL: 0 SRT, 1 TRT, 2 MRT, 4 SRT with the per-cell rate `om`
 // (rem = 1 - om, hw = 1 - 0.5 om as _core_py.py:133-134,181 compute them).
 // FORCE: 0 none, 1 Guo, 2 SimpleShift, 3 Guo with the force along x only.
-template <int Q, int MODEL, int FORCE>
-__device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p, double om = 0.0) {
+// MOUT: also hand back rho and the (shifted) velocity the collision used -
+// the macroscopic readout of the pre-collision state (k_fused_mom).
+template <int Q, int MODEL, int FORCE, bool MOUT = false>
+__device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p, double om = 0.0,
+                                             double* mout = nullptr) {
     using D = Dirs<Q>;
     constexpr bool GUO = FORCE == 1 || FORCE == 3;
     constexpr bool XO = FORCE == 3;
@@ -203,6 +206,12 @@ __device__ __forceinline__ void collide_cell(double (&f)[Q], const KParams& p, d
         ux = ux + p.sfx * inv_rho;
         uy = uy + p.sfy * inv_rho;
         uz = uz + p.sfz * inv_rho;
+    }
+    if constexpr (MOUT) {
+        mout[0] = rho;
+        mout[1] = ux;
+        mout[2] = uy;
+        mout[3] = uz;
     }
     const double usq15 = 1.5 * ((ux * ux + uy * uy) + uz * uz);
 

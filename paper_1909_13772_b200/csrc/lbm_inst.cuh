@@ -315,6 +315,34 @@ cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p,
     });
 }
 
+// fused sweep + readout of the pulled state (k_fused_mom): fp64 D3Q19 SRT /
+// TRT, unforced or Guo; cudaErrorNotSupported elsewhere (the caller then
+// runs the sweep and lbm_moments_planes as two launches)
+cudaError_t fused_mom(int q, int model, int force, const KGrid& g, const KParams& p,
+                      const void* src, void* dst, const uint32_t* cm, const uint32_t* tmk, int z0,
+                      int z1, double* rho, double* u, int* bad, cudaStream_t s) {
+    if constexpr (std::is_same_v<LBM_REAL, double>) {
+        if (q != 19 || (model != 0 && model != 1) || (force != 0 && force != 1 && force != 3) ||
+            p.mv_link || p.peer_lo || p.peer_hi)
+            return cudaErrorNotSupported;
+        if (z1 <= z0) return cudaSuccess;
+        dim3 b = fused_block(g.nx);
+        dim3 grid((g.nx + b.x - 1) / b.x, g.ny, z1 - z0);
+        auto go = [&](auto Mc, auto Fc) {
+            k_fused_mom<19, decltype(Mc)::value, decltype(Fc)::value><<<grid, b, 0, s>>>(
+                g, p, (const double*)src, (double*)dst, cm, tmk, z0, rho, u, bad);
+            return cudaGetLastError();
+        };
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        using I3 = std::integral_constant<int, 3>;
+        if (model == 0) return force == 0 ? go(I0{}, I0{}) : force == 1 ? go(I0{}, I1{}) : go(I0{}, I3{});
+        return force == 0 ? go(I1{}, I0{}) : force == 1 ? go(I1{}, I1{}) : go(I1{}, I3{});
+    } else {
+        return cudaErrorNotSupported;
+    }
+}
+
 cudaError_t collide_only(int q, int model, int force, const KGrid& g, const KParams& p, void* pdf,
                          const uint32_t* cm, int z0, int z1, cudaStream_t s) {
     if (model == LBM_SRT_FIELD) model = 4;

@@ -711,6 +711,74 @@ __global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, Real, MODEL, FO
     }
 }
 
+// k_fused that also writes the macroscopic readout of the state it pulls:
+// rho / u of R = S(src) per interior cell, exactly what k_moments with
+// stream_form = 1 gives for src (moments of the last sweep's pull instead of
+// a separate pass over the field).  Fluid cells take rho / u from the
+// collision itself (the same operations: sequential sums, u = m (1 / rho),
+// the Guo half shift when the sweep is Guo-forced); other cells sum their
+// pulled values.  fp64 storage, no moving walls, no fused halo.
+template <int Q, int MODEL, int FORCE>
+__global__ void __launch_bounds__(LBM_FUSED_BX, fused_minb_bx<Q, double, MODEL, FORCE>())
+    k_fused_mom(KGrid g, KParams p, const double* __restrict__ src, double* __restrict__ dst,
+                const uint32_t* __restrict__ cellmask, const uint32_t* __restrict__ typemask,
+                int z0, double* __restrict__ rho_out, double* __restrict__ u_out, int* bad) {
+    using D = Dirs<Q>;
+    constexpr bool GUO = FORCE == 1 || FORCE == 3;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = z0 + blockIdx.z;
+    const int xw0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    const bool edge_x = g.wrap_x && (xw0 == 0 || xw0 + 32 >= g.nx);
+    const bool edge_y = g.wrap_y && (y == 0 || y == g.ny - 1);
+    const bool edge_z = (g.zlo == LBM_ZFACE_WRAP && z == 0) || (g.zhi == LBM_ZFACE_WRAP && z == g.nz - 1);
+    const bool generic = edge_x || edge_y || edge_z;
+    if (x >= g.nx) return;
+    const int64_t cell = ((int64_t)z * g.ny + y) * g.nx + x;
+    const uint32_t code = cellmask ? __ldg(cellmask + cell) : LBM_MASK_FLUID;
+    prefetch_mask(g, cellmask, cell, (int64_t)g.nx * g.ny * g.nz);
+    double f[Q];
+    pull_cell<Q, double, double, 0>(g, p, src, x, y, z, code, typemask, generic, f);
+    double mo[4];
+    if (code & LBM_MASK_FLUID) {
+        collide_cell<Q, MODEL, FORCE, true>(f, p, 0.0, mo);
+    } else {
+        double rho = f[0];
+#pragma unroll
+        for (int i = 1; i < Q; ++i) rho = rho + f[i];
+        double mx = 0.0, my = 0.0, mz = 0.0;
+        static_for<0, Q>([&](auto I_) {
+            constexpr int i = decltype(I_)::value;
+            if constexpr (D::cx[i] == 1) mx = mx + f[i];
+            if constexpr (D::cx[i] == -1) mx = mx - f[i];
+            if constexpr (D::cy[i] == 1) my = my + f[i];
+            if constexpr (D::cy[i] == -1) my = my - f[i];
+            if constexpr (D::cz[i] == 1) mz = mz + f[i];
+            if constexpr (D::cz[i] == -1) mz = mz - f[i];
+        });
+        const double inv = 1.0 / rho;
+        mo[0] = rho;
+        mo[1] = mx * inv;
+        mo[2] = my * inv;
+        mo[3] = mz * inv;
+        if constexpr (GUO) {
+            mo[1] = mo[1] + p.sfx * inv;
+            mo[2] = mo[2] + p.sfy * inv;
+            mo[3] = mo[3] + p.sfz * inv;
+        }
+    }
+    if (mo[0] <= 0.0) atomicAdd(bad, 1);
+    rho_out[cell] = mo[0];
+    u_out[cell * 3 + 0] = mo[1];
+    u_out[cell * 3 + 1] = mo[2];
+    u_out[cell * 3 + 2] = mo[3];
+    double* dp = opaque(dst + lidx(g, z, 0, y, x));
+    static_for<0, Q>([&](auto I_) {
+        constexpr int i = decltype(I_)::value;
+        store_any<Q, i>(dp + g.dslot[i], f[i]);
+    });
+}
+
 // Two cells per thread, stacked in z (fp32 storage): both cells' 2Q pulls
 // are issued before the first cell is finished, so each warp keeps twice the
 // bytes in flight of k_fused with far fewer than twice the registers (the

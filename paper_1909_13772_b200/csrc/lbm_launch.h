@@ -14,6 +14,9 @@ struct KParams;
     cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p,             \
                       const void* src, void* dst, const uint32_t* cm, const uint32_t* tmk,       \
                       const uint64_t* lb, int z0, int z1, cudaStream_t s);                       \
+    cudaError_t fused_mom(int q, int model, int force, const KGrid& g, const KParams& p,         \
+                          const void* src, void* dst, const uint32_t* cm, const uint32_t* tmk,   \
+                          int z0, int z1, double* rho, double* u, int* bad, cudaStream_t s);     \
     cudaError_t collide_only(int q, int model, int force, const KGrid& g, const KParams& p,      \
                              void* pdf, const uint32_t* cm, int z0, int z1, cudaStream_t s);     \
     cudaError_t stream_only(int q, const KGrid& g, const KParams& p, const void* src,            \

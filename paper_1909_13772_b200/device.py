@@ -728,6 +728,10 @@ class DeviceLattice:
             lb = masks.linkbits(self)
         sp = self._sp(main)
         launches = 0
+        # the last sweep also writes the readout (lbm_fused_step_moments) -
+        # not with the link-bit map (its kernels read the cell mask);
+        # LBM_B200_JOB_FUSE_MOMENTS=0 keeps the separate moments pass
+        fuse_mom = lb is None and os.environ.get("LBM_B200_JOB_FUSE_MOMENTS", "1") != "0"
         for act in job_plan(nz, steps, chunk):
             if act[0] == "fill":
                 _, ci, z0, z1 = act
@@ -737,6 +741,17 @@ class DeviceLattice:
                 _lib.call("lbm_fill_collide_planes", self.gref, kp.ref, _lib.ptr(st["rho"]),
                           _lib.ptr(st["u"]), z0, z1, _lib.ptr(buf[c0]), _lib.ptr(buf[1 - c0]),
                           _lib.ptr(masks.cellmask), sp)
+            elif act[0] == "step" and act[1] == steps and fuse_mom:
+                # the last sweep reads G_{K-1}: it hands back the moments of
+                # R_K = S(G_{K-1}) on the same planes (job_plan gives the
+                # moments exactly this step's ranges)
+                _, n, z0, z1 = act
+                _lib.call("lbm_fused_step_moments", self.gref, kp.ref, kp_mom.ref,
+                          _lib.ptr(buf[(c0 + n - 1) % 2]), _lib.ptr(buf[(c0 + n) % 2]),
+                          _lib.ptr(masks.cellmask), _lib.ptr(masks.typemask),
+                          z0, z1, _lib.ptr(st["rho_o"]), _lib.ptr(st["u_o"]),
+                          _lib.ptr(st["bad"]), sp)
+                launches += 1
             elif act[0] == "step":
                 _, n, z0, z1 = act
                 _lib.call("lbm_fused_step_bits", self.gref, kp.ref,
@@ -745,10 +760,11 @@ class DeviceLattice:
                 launches += 1
             else:
                 _, z0, z1 = act
-                _lib.call("lbm_moments_planes", self.gref, kp_mom.ref,
-                          _lib.ptr(buf[(c0 + steps - 1) % 2]), _lib.ptr(masks.cellmask),
-                          _lib.ptr(masks.typemask), 1, z0, z1, _lib.ptr(st["rho_o"]),
-                          _lib.ptr(st["u_o"]), _lib.ptr(st["bad"]), sp)
+                if not fuse_mom:
+                    _lib.call("lbm_moments_planes", self.gref, kp_mom.ref,
+                              _lib.ptr(buf[(c0 + steps - 1) % 2]), _lib.ptr(masks.cellmask),
+                              _lib.ptr(masks.typemask), 1, z0, z1, _lib.ptr(st["rho_o"]),
+                              _lib.ptr(st["u_o"]), _lib.ptr(st["bad"]), sp)
                 evm = torch.cuda.Event()
                 evm.record(main)
                 dn.wait_event(evm)

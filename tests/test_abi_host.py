@@ -26,7 +26,7 @@ def test_library_loads_and_exports_every_header_symbol():
     assert sorted(syms) == sorted(_lib.EXPORTS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.lbm_abi_version() == _lib.ABI_VERSION == 7
+    assert lib.lbm_abi_version() == _lib.ABI_VERSION == 8
 
 
 def test_library_is_sm100a():
@@ -271,6 +271,14 @@ def test_job_plan_respects_the_sweep_dependencies(nz, steps, chunk):
     plan = job_plan(nz, steps, chunk)
     bounds, _ = job_schedule(nz, steps, chunk)
     assert [a[2:] for a in plan if a[0] == "fill"] == bounds
+    # the moments of each round cover exactly the last sweep's planes of that
+    # round (run_job fuses them into that launch, lbm_fused_step_moments)
+    last = {}
+    for act in plan:
+        if act[0] == "step" and act[1] == steps:
+            last["range"] = act[2:]
+        elif act[0] == "moments":
+            assert last.pop("range") == act[1:], act
     ver = np.full(nz, -1)                 # ver[p]: newest G_n written on plane p
     reads = {}                            # (n, p): readers of G_n on p still to come
     moments = np.zeros(nz, dtype=bool)
