@@ -317,11 +317,19 @@ cudaError_t fused(int q, int model, int force, const KGrid& g, const KParams& p,
 
 // fused sweep + readout of the pulled state (k_fused_mom): fp64 D3Q19 SRT /
 // TRT, unforced or Guo; cudaErrorNotSupported elsewhere (the caller then
-// runs the sweep and lbm_moments_planes as two launches)
-cudaError_t fused_mom(int q, int model, int force, const KGrid& g, const KParams& p,
-                      const void* src, void* dst, const uint32_t* cm, const uint32_t* tmk, int z0,
-                      int z1, double* rho, double* u, int* bad, cudaStream_t s) {
-    if constexpr (std::is_same_v<LBM_REAL, double>) {
+// runs the sweep and lbm_moments_planes as two launches).  A template on the
+// storage type, so the fp32 unit (built with -fmad=true) never instantiates
+// k_fused_mom: an `if constexpr` in a plain function still instantiates its
+// discarded branch, and a kernel compiled into both units shares one host
+// stub - which copy a launch resolves to then depends on which module the
+// lazy loader brought in first (measured: the contracted copy gave 1-ulp
+// velocity differences after fp32 kernels had run in the same process).
+template <typename R>
+static cudaError_t fused_mom_t(int q, int model, int force, const KGrid& g, const KParams& p,
+                               const void* src, void* dst, const uint32_t* cm,
+                               const uint32_t* tmk, int z0, int z1, double* rho, double* u,
+                               int* bad, cudaStream_t s) {
+    if constexpr (std::is_same_v<R, double>) {
         if (q != 19 || (model != 0 && model != 1) || (force != 0 && force != 1 && force != 3) ||
             p.mv_link || p.peer_lo || p.peer_hi)
             return cudaErrorNotSupported;
@@ -341,6 +349,12 @@ cudaError_t fused_mom(int q, int model, int force, const KGrid& g, const KParams
     } else {
         return cudaErrorNotSupported;
     }
+}
+
+cudaError_t fused_mom(int q, int model, int force, const KGrid& g, const KParams& p,
+                      const void* src, void* dst, const uint32_t* cm, const uint32_t* tmk, int z0,
+                      int z1, double* rho, double* u, int* bad, cudaStream_t s) {
+    return fused_mom_t<LBM_REAL>(q, model, force, g, p, src, dst, cm, tmk, z0, z1, rho, u, bad, s);
 }
 
 cudaError_t collide_only(int q, int model, int force, const KGrid& g, const KParams& p, void* pdf,

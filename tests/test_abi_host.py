@@ -40,6 +40,25 @@ def test_library_is_sm100a():
     assert "sm_100a" in out.stdout
 
 
+def test_no_kernel_in_two_units():
+    """Every kernel is compiled into exactly one unit.  The units differ in
+    -fmad (fp64 bitwise units: false, fp32 unit: true) and a kernel in two
+    of them shares one host stub, so which copy a launch runs would depend on
+    module load order (a fused readout once ran its contracted fp32-unit copy
+    and came out 1 ulp off)."""
+    import collections
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(exe).exists():
+        pytest.skip("cuobjdump unavailable")
+    out = subprocess.run([exe, "-symbols", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    names = [ln.split()[-1] for ln in out.stdout.splitlines() if "STO_ENTRY" in ln]
+    assert len(names) > 100
+    dup = [n for n, c in collections.Counter(names).items() if c > 1]
+    assert not dup, f"kernels compiled into more than one unit: {dup[:5]}"
+
+
 def test_slot_layout_groups_directions_by_cz():
     lib = _lib.load()
     for name in ("D2Q9", "D3Q19", "D3Q27"):

@@ -20,6 +20,31 @@ def _lattice(config, dtype, cells):
     return P, forest, pdf, handling, model, force, dims
 
 
+def _host_moments(pdf, force):
+    """rho / u of R_K (the state the readout reads) in numpy, the reference's
+    macroscopic() (lbm/collision.py:157-184) op for op: sequential density,
+    momentum in index order, u = m (1 / rho) (+ (F / 2) (1 / rho) for Guo)."""
+    import paper_1909_13772_b200 as P
+    kind, dev = pdf.lattice.readout_device()
+    f = dev.cpu().numpy()
+    if kind == "full":
+        f = f[:, 1:-1, 1:-1, 1:-1]
+    c = np.asarray(pdf.stencil.c)
+    rho = f[0].copy()
+    for i in range(1, f.shape[0]):
+        rho = rho + f[i]
+    m = np.zeros(rho.shape + (3,))
+    for i in range(f.shape[0]):
+        for a in range(3):
+            if c[i][a]:
+                m[..., a] += c[i][a] * f[i]
+    inv = (1.0 / rho)[..., None]
+    u = m * inv
+    if isinstance(force, P.Guo):
+        u = u + 0.5 * np.asarray(force.force) * inv
+    return rho, u
+
+
 CASES = [
     ("c4", "f64", (64, 48, 40), 7, 8),
     ("c4", "f64", (64, 48, 40), 1, 5),
@@ -54,16 +79,36 @@ def test_run_arrays_bitwise_vs_call_sequence(config, dtype, cells, steps, chunk)
                 P.stream_collide(pdf, model, force=force, handling=handling)
             P.macroscopic_arrays(pdf, force=force, out=out)
         first = (out[0].numpy().copy(), out[1].numpy().copy())
+        host = _host_moments(pdf, force)
+        m = pdf.lattice.stream_masks
+        fluid = (m.cellmask.cpu().numpy() & 1).astype(bool) if m is not None else None
         # the end state continues exactly like the sequence's
         for _ in range(3):
             P.stream_collide(pdf, model, force=force, handling=handling)
         kind, dev = pdf.lattice.readout_device()
         rho2, u2 = P.macroscopic_arrays(pdf, force=force)
         runs.append((first, dev.cpu().numpy(), rho2.cpu().numpy(), u2.cpu().numpy(),
-                     pdf.lattice.steps))
+                     pdf.lattice.steps, host, fluid))
         del pdf, forest, handling
-    (a_first, a_pdf, a_rho, a_u, a_steps), (b_first, b_pdf, b_rho, b_u, b_steps) = runs
+    (a_first, a_pdf, a_rho, a_u, a_steps, a_host, fluid), \
+        (b_first, b_pdf, b_rho, b_u, b_steps, b_host, _) = runs
     assert a_steps == b_steps == steps + 3
+    assert a_host[0].tobytes() == b_host[0].tobytes() and a_host[1].tobytes() == b_host[1].tobytes(), \
+        "R_K after the job"
+    # both readouts against the reference formula on the host (collision.py:157-184);
+    # fp64 NoSlip tiles only (fp32 readouts widen centred populations, and the
+    # UBB lid's R_K carries the wall term the host copy of S(G) does not)
+    checks = (("call sequence", a_first), ("run_arrays", b_first)) \
+        if dtype == "f64" and config in ("c4", "c1") else ()
+    for name, first in checks:
+        nr = int((first[0] != a_host[0]).sum())
+        du = (first[1] != a_host[1]).any(-1)
+        nu = int(du.sum())
+        where = "" if fluid is None else \
+            f" ({int((du & fluid).sum())} fluid, {int((du & ~fluid).sum())} of {int((~fluid).sum())} non-fluid)"
+        assert nr == 0 and nu == 0, (
+            f"{name}: {nr} rho / {nu} u cells differ from the host readout{where}, "
+            f"max |du| {float(np.abs(first[1] - a_host[1]).max()):.3e}")
     assert a_first[0].tobytes() == b_first[0].tobytes(), "rho after the job"
     assert a_first[1].tobytes() == b_first[1].tobytes(), "u after the job"
     assert a_pdf.tobytes() == b_pdf.tobytes(), "PDFs three sweeps after the job"
